@@ -1,0 +1,395 @@
+"""Benchmark of the decoupled-PPO training hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config cfg2|cfg1|cfg3|cfg5]
+
+One step = one pass of the hot path over one synthetic global batch of the
+named shape: K3 advantages, K4/K5 allocation + packing of every minibatch, K1
+prox log-probs over every token, then per minibatch K2 (fused decoupled-PPO
+loss + backward -> dlogits) over every micro-batch and one NCCL all-reduce of
+the statistics (N > 1).  The model is out of scope: its logits are synthetic
+bf16 tensors resident in HBM (rotating 10 GB buffers, larger than L2, so no L2
+flush is needed) handed to the hot path through the same callback a real model
+would use.  Prints ONE JSON line on rank 0.
+
+``--impl reference`` times the reference algorithm on the host CPU (the float64
+numpy oracle restating trainer.py, all cores) on a bounded sample of the same
+workload; only rank 0 works under torchrun.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import multiprocessing as mp
+import os
+import platform
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "packed tokens/sec for logprob+decoupled-PPO fwd/bwd; % HBM roofline"
+
+CONFIGS = {
+    # BASELINE.json configs[1]: the headline single-GPU workload
+    "cfg2": dict(workload="Qwen2-1.5B shape (BASELINE configs[1])", vocab=151936, rollouts=512,
+                 prompts=128, len_lo=128, len_hi=8192, dtype="bf16", budget=32768,
+                 minibatches=4),
+    # configs[0]: CPU-reference synthetic case
+    "cfg1": dict(workload="CPU-ref synthetic (BASELINE configs[0])", vocab=32000, rollouts=64,
+                 prompts=16, len_lo=128, len_hi=2048, dtype="fp32", budget=32768, minibatches=4),
+    # configs[2]: Qwen2-7B shape, eta=4 staleness mask
+    "cfg3": dict(workload="Qwen2-7B shape (BASELINE configs[2])", vocab=152064, rollouts=1024,
+                 prompts=256, len_lo=128, len_hi=27648, dtype="bf16", budget=32768,
+                 minibatches=4, eta=4),
+}
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+    except Exception:
+        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+def workload_arrays(cfg, n_copies=1, seed=0):
+    """Synthetic rollouts: lengths U[lo, hi], tokens uniform, rewards +-5, prompt groups."""
+    rng = np.random.default_rng(seed)
+    n = cfg["rollouts"] * n_copies
+    lengths = rng.integers(cfg["len_lo"], cfg["len_hi"] + 1, size=n)
+    bounds = np.concatenate([[0], np.cumsum(lengths)]).astype(np.int64)
+    T = int(bounds[-1])
+    tokens = rng.integers(0, cfg["vocab"], size=T, dtype=np.int64)
+    rewards = rng.choice([5.0, -5.0], size=n)
+    per = cfg["rollouts"] // cfg["prompts"]
+    group_ids = (np.arange(n) // per).astype(np.int32)
+    eta = cfg.get("eta", 0)
+    start_ver = 100 - rng.integers(0, eta + 1, size=n)
+    versions = np.repeat(start_ver, lengths).astype(np.int32)
+    return dict(bounds=bounds, tokens=tokens, rewards=rewards, group_ids=group_ids,
+                versions=versions, T=T, n=n)
+
+
+# ------------------------------------------------------------------ CPU baseline (oracle)
+def _cpu_worker(job):
+    seed, rows, V = job
+    import oracle as O
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal((rows, V), dtype=np.float32) * 2.0
+    x = (x.view(np.uint32) & 0xFFFF0000).view(np.float32).astype(np.float64)  # bf16 values
+    tok = rng.integers(0, V, size=rows)
+    t0 = time.perf_counter()
+    lp = O.token_logprobs(x, tok)           # K1: prox log-probs (trainer.py:128-137)
+    O.token_entropy(x)
+    prox = lp + rng.normal(0, 0.02, size=rows)
+    behav = prox + rng.normal(0, 0.1, size=rows)
+    adv = rng.normal(size=rows)
+    O.surrogate_terms(x, tok, behav, prox, adv)  # K2: loss + dlogits (trainer.py:150-195)
+    return rows, time.perf_counter() - t0
+
+
+def cpu_baseline(V, target_s=10.0, workers=None):
+    """Oracle K1+K2 math on a bounded sample, one process per host core."""
+    workers = workers or os.cpu_count() or 1
+    r, dt = _cpu_worker((12345, 2, V))
+    per_row = dt / 2
+    mem_rows = max(1, int(24e9 / (V * 8 * 8) / workers))
+    rows = int(max(2, min(512, mem_rows, target_s / max(per_row, 1e-6))))
+    ctx = mp.get_context("fork")
+    t0 = time.perf_counter()
+    with ctx.Pool(workers) as pool:
+        res = pool.map(_cpu_worker, [(1000 + i, rows, V) for i in range(workers)])
+    wall = time.perf_counter() - t0
+    done = sum(x[0] for x in res)
+    cpu = platform.processor() or ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            cpu = next((l.split(":", 1)[1].strip() for l in f if l.startswith("model name")), cpu)
+    except OSError:
+        pass
+    return dict(value=done / wall, unit="tokens/s", cores=workers, kind="port",
+                sample=f"{done} tokens ({workers} procs x {rows} rows) of V={V} bf16-valued "
+                       f"logits through the float64 numpy oracle (K1 logprob+entropy, K2 "
+                       f"loss+dlogits); host: {cpu}",
+                wall_s=wall)
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    V = cfg["vocab"]
+    times, vals = [], []
+    base = None
+    for i in range(args.warmup + args.steps):
+        b = cpu_baseline(V, target_s=args.ref_seconds)
+        if i >= args.warmup:
+            times.append(b["wall_s"])
+            vals.append(b["value"])
+            base = b
+    value = float(np.mean(vals))
+    line = dict(metric=METRIC, value=value, unit="tokens/s", n_gpus=args.gpus, steps=args.steps,
+                warmup=args.warmup, ms_per_step=1e3 * float(np.mean(times)),
+                higher_is_better=True, scaling="weak", vs_baseline=None, dtype="f64",
+                data="synthetic", impl="reference",
+                config=dict(workload=cfg["workload"], vocab=V, note="bounded CPU sample per step"),
+                cpu_baseline=dict(value=value, unit="tokens/s", cores=base["cores"],
+                                  kind=base["kind"], sample=base["sample"]),
+                e2e=dict(value=value, unit="tokens/s", h2d_bytes_per_step=0,
+                         d2h_bytes_per_step=0))
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ clocks sampler
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}",
+                                      f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return dict(sm_mhz=None, sm_max_mhz=None, reasons=["nvidia-smi unavailable"], samples=0)
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 4 + i and r[4 + i].lower() == "active"})
+        return dict(sm_mhz=float(np.median(sm)) if sm else None,
+                    sm_max_mhz=max(mx) if mx else None, reasons=reasons, samples=len(self.rows))
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    cpu_base = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu_base = cpu_baseline(cfg["vocab"], target_s=args.cpu_seconds)  # before CUDA init
+        cpu_base.pop("wall_s", None)
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2505_24298_b200 import kernels as K
+    from paper_2505_24298_b200.hotpath import DecoupledPPOStep, HotPathConfig, PackedRollouts
+
+    # weak scaling: the global batch is N copies of the config's batch shape
+    W = workload_arrays(cfg, n_copies=world)
+    V = cfg["vocab"]
+    ldt = torch.bfloat16 if cfg["dtype"] == "bf16" else torch.float32
+    C = cfg["budget"]
+    hp = HotPathConfig(minibatches=cfg["minibatches"], micro_token_budget=C,
+                       micro_min_groups=max(1, world), eta_mask=cfg.get("eta", -1) if "eta" in cfg else -1)
+    runner = DecoupledPPOStep(hp, dev)
+
+    # synthetic model outputs: rotating logits buffers (> L2) + one dlogits buffer
+    n_buf = args.logit_buffers
+    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
+    bufs = []
+    for _ in range(n_buf):
+        b = torch.empty((C, V), dtype=ldt, device=dev)
+        b.normal_(0.0, 2.0, generator=gen)
+        bufs.append(b)
+    dl_buf = torch.empty((C, V), dtype=ldt, device=dev)
+    counter = [0]
+
+    def logits_fn(phase, m, g, rows):
+        b = bufs[counter[0] % n_buf]
+        counter[0] += 1
+        return b[: rows.numel()]
+
+    def dlogits_fn(m, g, logits):
+        return dl_buf[: logits.shape[0]]
+
+    # pinned host copies (e2e path) and device-resident copies (value path)
+    pin = lambda a: torch.from_numpy(a).pin_memory()
+    host = dict(traj_bounds=pin(W["bounds"]), tokens=pin(W["tokens"]),
+                behav=pin(np.zeros(W["T"])), rewards=pin(W["rewards"]),
+                versions=pin(W["versions"]) if "eta" in cfg else None)
+    ro = PackedRollouts.from_host(**host, device=dev)
+    torch.cuda.synchronize()
+
+    def step(r):
+        counter[0] = 0
+        return runner.run(r, logits_fn, dlogits_fn=dlogits_fn, current_version=100)
+
+    # one pass to get prox under the synthetic logits, then behaviour = prox + noise
+    runner.record_events = False
+    sp = runner.plan(ro)
+    counter[0] = 0
+    prox = runner.prox_logprobs(ro, sp, logits_fn)
+    if world > 1:
+        dist.all_reduce(prox)  # each token's prox lives on one rank (others hold garbage)
+    noise = torch.randn(W["T"], dtype=torch.float64, device=dev,
+                        generator=torch.Generator(device=dev).manual_seed(7)) * 0.1
+    behav = prox + noise
+    ro.behav.copy_(behav)
+    host["behav"].copy_(behav.cpu())
+    torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step(ro)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    # ---------------- timed region: device-resident inputs
+    runner.launches = 0
+    runner.k1_events, runner.k2_events = [], []
+    runner.k1_bytes = runner.k2_bytes = 0
+    runner.record_events = True
+    s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        s_ev.record()
+        for _ in range(args.steps):
+            res = step(ro)
+        e_ev.record()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    runner.record_events = False
+    ms = s_ev.elapsed_time(e_ev) / args.steps
+    launches = runner.launches // args.steps
+    k2_ms = sum(s.elapsed_time(e) for s, e in runner.k2_events)
+    k1_ms = sum(s.elapsed_time(e) for s, e in runner.k1_events)
+    k2_bytes, k1_bytes = runner.k2_bytes, runner.k1_bytes
+    n_k2 = len(runner.k2_events)
+
+    # ---------------- e2e: public API with pinned host inputs and a D2H of the result
+    e2e_steps = max(1, args.e2e_steps)
+    res_host = torch.empty((cfg["minibatches"], 8), dtype=torch.float64).pin_memory()
+    s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    s2.record()
+    h2d = d2h = 0
+    for _ in range(e2e_steps):
+        r = PackedRollouts.from_host(**host, device=dev)
+        h2d = r.h2d_bytes()
+        out = step(r)  # returns host stats (one D2H of the minibatch sums)
+        d2h = out.minibatch_stats.nbytes
+    e2.record()
+    torch.cuda.synchronize()
+    e2e_ms = s2.elapsed_time(e2) / e2e_steps
+    del res_host
+
+    t_max = torch.tensor([ms, e2e_ms, k2_ms, k1_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    ms, e2e_ms = float(t_max[0]), float(t_max[1])
+    T = W["T"]
+    if rank == 0:
+        peak, peak_src = _peaks()
+        k2_gbs = (k2_bytes / (k2_ms * 1e-3)) / 1e9 if k2_ms > 0 else 0.0
+        k1_gbs = (k1_bytes / (k1_ms * 1e-3)) / 1e9 if k1_ms > 0 else 0.0
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tp):
+            try:
+                with open(tp) as f:
+                    traffic = json.load(f).get("k2_dram_bytes_per_launch")
+            except Exception:
+                traffic = None
+        es = 2 if ldt == torch.bfloat16 else 4
+        line = dict(
+            metric=METRIC, value=T / (ms * 1e-3), unit="tokens/s", n_gpus=world,
+            steps=args.steps, warmup=args.warmup, ms_per_step=ms, higher_is_better=True,
+            scaling="weak", vs_baseline=None, dtype=cfg["dtype"],
+            data="synthetic (random bf16 logits in rotating HBM buffers; rollouts seeded)",
+            config=dict(workload=cfg["workload"], vocab=V, rollouts=W["n"], tokens=T,
+                        lengths=f"U[{cfg['len_lo']},{cfg['len_hi']}] seed 0",
+                        micro_token_budget=C, minibatches=cfg["minibatches"],
+                        micro_min_groups=hp.micro_min_groups, logits_dtype=cfg["dtype"],
+                        l2="inputs > L2: %d rotating %.1f GB logits buffers" % (
+                            n_buf, C * V * es / 1e9),
+                        parallelism=f"dp{world}", micro_batches=res.microbatches),
+            roofline=dict(bound="hbm", kernel="areal_ppo_fwd_bwd (K2, row_ring)",
+                          achieved=k2_gbs, peak=peak, unit="GB/s", frac=k2_gbs / peak,
+                          traffic=traffic, peak_source=peak_src,
+                          algorithmic_bytes_per_token=2 * V * es + 52,
+                          launches=n_k2, avg_launch_ms=k2_ms / max(n_k2, 1)),
+            k1=dict(kernel="areal_logprob_fwd (K1)", achieved_gbs=k1_gbs, frac=k1_gbs / peak,
+                    bytes_per_token=V * es + 16, ms_per_step=k1_ms / args.steps),
+            k2=dict(ms_per_step=k2_ms / args.steps, tokens_per_s=T / (k2_ms / args.steps * 1e-3)),
+            e2e=dict(value=T / (e2e_ms * 1e-3), unit="tokens/s", h2d_bytes_per_step=h2d,
+                     d2h_bytes_per_step=d2h,
+                     note="public API DecoupledPPOStep.run from pinned host rollouts; "
+                          "logits are device-resident model outputs"),
+            gpu_launches=launches,
+            clocks=clk.summary(),
+            cpu_baseline=cpu_base,
+            loss=res.loss, clip_fraction=res.clip_fraction,
+        )
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--logit-buffers", type=int, default=3)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--ref-seconds", type=float, default=6.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

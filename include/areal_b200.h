@@ -1,0 +1,182 @@
+/*
+ * areal_b200.h — C-ABI of the B200-native decoupled-PPO training hot path.
+ *
+ * Built from paper_2505_24298_b200/csrc/ into libareal_b200.so (sm_100a).
+ * Every entry point takes plain device pointers, sizes and a cudaStream_t
+ * passed as void*; kernels are stream-ordered and asynchronous, the library
+ * never allocates device memory (callers pass workspaces) and never
+ * synchronises except where noted.  No torch types cross this boundary.
+ *
+ * The reference (asyncrl, pure numpy) has no FFI; its drop-in boundary is the
+ * Python module API of /root/reference/pkg/src/asyncrl/trainer.py.  Each entry
+ * below names the reference function(s) it replaces; the Python mirror
+ * paper_2505_24298_b200/trainer.py keeps the reference's names and semantics
+ * on top of these calls (see INTEGRATION.md for the ctypes binding).
+ *
+ * Conventions
+ *   - dtype codes: areal_dtype_t.  Logits/dlogits share one dtype.
+ *   - per-token float arrays (behav, prox, adv, lp, entropy) are float64 and
+ *     indexed by the GLOBAL token index; `row_index` (int32, may be NULL =
+ *     identity) maps a logits row r to that global index, so a packed
+ *     micro-batch never needs a gather pass over the per-token arrays.
+ *   - status: 0 = OK, otherwise an areal_status_t; areal_status_string()
+ *     gives the text.  Input validation that needs device data (allocator
+ *     lengths) is reported through a device status array.
+ */
+#ifndef AREAL_B200_H_
+#define AREAL_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AREAL_ABI_VERSION 1
+#define AREAL_N_STATS 8
+/* Workspace every K1/K2/K3 call needs (per concurrently used stream), zeroed once
+ * at allocation.  K2 uses the lower half (ticket counter + per-CTA partials, left
+ * zeroed after each launch), K3 the upper half (scratch). */
+#define AREAL_WORKSPACE_BYTES (1u << 20)
+/* Largest number of sequences one minibatch may hold in the allocator. */
+#define AREAL_MAX_ITEMS_PER_MINIBATCH 8192
+
+typedef enum {
+  AREAL_OK = 0,
+  AREAL_ERR_INVALID_ARGUMENT = 1,
+  AREAL_ERR_BAD_DTYPE = 2,
+  AREAL_ERR_BAD_SHAPE = 3,
+  AREAL_ERR_MISALIGNED = 4,
+  AREAL_ERR_LEN_NONPOSITIVE = 5,     /* trainer.py:249-250 */
+  AREAL_ERR_LEN_EXCEEDS_CAPACITY = 6,/* trainer.py:251-252 */
+  AREAL_ERR_MIN_GROUPS = 7,          /* trainer.py:246-247 */
+  AREAL_ERR_WORKSPACE = 8,
+  AREAL_ERR_CUDA = 9,
+  AREAL_ERR_UNSUPPORTED = 10,
+  AREAL_ERR_BAD_CLIP_EPS = 11        /* trainer.py:48-49 */
+} areal_status_t;
+
+typedef enum { AREAL_F32 = 0, AREAL_BF16 = 1, AREAL_F16 = 2, AREAL_F64 = 3 } areal_dtype_t;
+
+/* Kernel selection for K1/K2.  AUTO picks ROW_RING (TMA bulk ring, row kept
+ * resident in shared memory, thread-block cluster split for long rows) when
+ * the row is large and 16-byte aligned, else ROW_WARP (one warp per row). */
+typedef enum { AREAL_ALGO_AUTO = 0, AREAL_ALGO_ROW_WARP = 1, AREAL_ALGO_ROW_RING = 2 } areal_algo_t;
+
+/* Order of the float64 statistics vector (accumulated with +=). */
+typedef enum {
+  AREAL_STAT_OBJECTIVE_SUM = 0, /* trainer.py:188 */
+  AREAL_STAT_N_VALID = 1,       /* trainer.py:191 */
+  AREAL_STAT_N_CLIPPED = 2,     /* trainer.py:186, 192 */
+  AREAL_STAT_RATIO_SUM = 3,     /* trainer.py:193 */
+  AREAL_STAT_N_EXCLUDED = 4,    /* trainer.py:194 */
+  AREAL_STAT_N_MASKED = 5,      /* extension: version-staleness / behaviour-cap mask */
+  AREAL_STAT_ENTROPY_SUM = 6,   /* extension: sum of H_t over valid tokens */
+  AREAL_STAT_N_TOKENS = 7
+} areal_stat_t;
+
+typedef struct {
+  double clip_eps;          /* epsilon of clip(u, 1-eps, 1+eps); (0,1)           */
+  double behav_weight_cap;  /* > 0: mask tokens with prox/behav weight > cap     */
+  double grad_scale;        /* dlogits = grad_scale * coef * (softmax - onehot)  */
+  int32_t decoupled;        /* 1: decoupled objective, 0: naive (trainer.py:165-170) */
+  int32_t eta_mask;         /* >= 0: mask tokens with cur_version - version > eta */
+  int32_t current_version;  /* policy version being optimised                    */
+  int32_t algo;             /* areal_algo_t                                       */
+} areal_ppo_params_t;
+
+typedef enum { AREAL_ADV_REFERENCE = 0, AREAL_ADV_GAE = 1 } areal_adv_mode_t;
+typedef enum {
+  AREAL_NORM_NONE = 0,
+  AREAL_NORM_GLOBAL = 1,          /* token-weighted, numpy-exact (trainer.py:119-123) */
+  AREAL_NORM_GROUP_TOKEN = 2,     /* GRPO, token-weighted per group                  */
+  AREAL_NORM_GROUP_SEQUENCE = 3   /* GRPO, one value per trajectory                  */
+} areal_norm_t;
+
+typedef struct {
+  double gamma;   /* GAE discount (reference: 1)   */
+  double lam;     /* GAE lambda   (reference: 1)   */
+  double eps;     /* group norm: (x - mean) / (std + eps) */
+  int32_t mode;   /* areal_adv_mode_t */
+  int32_t norm;   /* areal_norm_t     */
+} areal_adv_params_t;
+
+/* ---- library info ------------------------------------------------------- */
+int areal_abi_version(void);
+const char* areal_status_string(int status);
+/* Number of stats slots a K2 launch uses in the workspace (diagnostics). */
+size_t areal_workspace_bytes(void);
+
+/* ---- K1: log-softmax-gather (+ entropy) ----------------------------------
+ * Replaces recompute_prox_logprobs (trainer.py:128-137) ->
+ * batch_token_log_probs (policy.py:159-163) -> log_softmax (policy.py:145-147)
+ * on given logits.  lp_out[idx] = x_r[a] - logsumexp(x_r); entropy_out may be
+ * NULL.  Reads each logits row once. */
+int areal_logprob_fwd(const void* logits, int64_t ld_logits, int dtype, int64_t n_rows,
+                      int64_t vocab, const int64_t* tokens, const int32_t* row_index,
+                      double* lp_out, double* entropy_out, int algo,
+                      void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- K2: decoupled / naive PPO loss fused with its backward ---------------
+ * Replaces _surrogate_terms (trainer.py:150-195) minus the model GEMMs, and
+ * the per-token part of _ppo_loss (198-213).  Writes dlogits (may alias
+ * logits for an in-place backward), lp/entropy per token (either may be NULL)
+ * and accumulates AREAL_N_STATS float64 statistics into `stats` (device).
+ * Deterministic: per-CTA partials reduced in a fixed order. */
+int areal_ppo_fwd_bwd(const void* logits, int64_t ld_logits, void* dlogits, int64_t ld_dlogits,
+                      int dtype, int64_t n_rows, int64_t vocab, const int64_t* tokens,
+                      const double* behav, const double* prox, const double* adv,
+                      const int32_t* versions, const int32_t* row_index,
+                      const areal_ppo_params_t* params, double* lp_out, double* entropy_out,
+                      double* stats, void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- K3: advantages --------------------------------------------------------
+ * Replaces compute_advantages (trainer.py:114-125).  REFERENCE mode with
+ * GLOBAL norm is bit-identical to the reference (numpy pairwise summation is
+ * replayed).  GAE mode runs a per-sequence reverse scan (values may be NULL);
+ * group norms use group_ids[n_traj] in [0, n_groups).  norm_stats_out (device,
+ * 2 doubles, may be NULL) receives the global mean and std. */
+int areal_advantages(const double* rewards, const int64_t* traj_bounds, int64_t n_traj,
+                     int64_t n_tokens, const double* values, const int32_t* group_ids,
+                     int32_t n_groups, const areal_adv_params_t* params, double* adv_out,
+                     double* returns_out, double* norm_stats_out, void* workspace,
+                     size_t workspace_bytes, void* stream);
+
+/* ---- K4 + K5a: dynamic micro-batch allocation and packing plan -------------
+ * Replaces allocate_microbatches (trainer.py:235-270) for M minibatches at
+ * once, plus the packing order of train_step (trainer.py:310-320).
+ * Items (non-empty trajectories) of minibatch m are item_traj[mb_offsets[m] ..
+ * mb_offsets[m+1]) (device); their lengths come from traj_bounds.
+ * Outputs (device):
+ *   group_of/slot_of[n_items]    group and placement slot of each item
+ *   n_groups[M]
+ *   group_cu[n_items + M]        token boundaries of micro-batches in the packed
+ *                                stream; minibatch m uses entries
+ *                                [mb_offsets[m] + m, ... + n_groups[m]]
+ *   group_seq_cu[n_items + M]    same layout, in packed-sequence units
+ *   packed_traj[n_items]         trajectory id at each packed sequence position
+ *   seq_cu[n_items + 1]          cu_seqlens of the whole packed stream
+ *   status[M]                    0 or an areal_status_t (lengths check)
+ * mb_token_start[M] (device) is the packed-stream offset of each minibatch. */
+int areal_plan_microbatches(const int64_t* traj_bounds, const int32_t* item_traj,
+                            const int32_t* mb_offsets, const int64_t* mb_token_start,
+                            int32_t n_minibatches, int32_t n_items, int32_t max_items_per_mb,
+                            int64_t capacity, int32_t min_groups, int32_t* group_of,
+                            int32_t* slot_of, int32_t* n_groups, int64_t* group_cu,
+                            int32_t* group_seq_cu, int32_t* packed_traj, int64_t* seq_cu,
+                            int32_t* status, void* stream);
+
+/* ---- K5b: packed gather index ----------------------------------------------
+ * gather[p] = global token index of packed position p (p < seq_cu[n_items]),
+ * i.e. np.concatenate([token_range(traj) for traj in packed order])
+ * (trainer.py:320).  Also writes the token's packed-sequence id if seq_id is
+ * non-NULL. */
+int areal_fill_gather(const int64_t* traj_bounds, const int32_t* packed_traj,
+                      const int64_t* seq_cu, int32_t n_items, int64_t n_packed_tokens,
+                      int32_t* gather, int32_t* seq_id, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AREAL_B200_H_ */

@@ -1,0 +1,204 @@
+// common.cuh — dtype traits and sm_100a PTX helpers shared by the hot-path kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+#include "../../include/areal_b200.h"
+
+#define AREAL_CUDA_CHECK_LAUNCH()                    \
+  do {                                               \
+    cudaError_t _e = cudaGetLastError();             \
+    if (_e != cudaSuccess) return AREAL_ERR_CUDA;    \
+  } while (0)
+
+namespace areal {
+
+constexpr int kWarp = 32;
+
+// ------------------------------------------------------------------ dtype traits
+// Acc is the accumulation type of the row reductions: fp32 for 16/32-bit
+// logits, fp64 for fp64 logits (the drop-in parity path).
+template <typename T> struct Traits;
+template <> struct Traits<float> {
+  using Acc = float;
+  static __device__ __forceinline__ float to_acc(float v) { return v; }
+  static __device__ __forceinline__ float from_acc(float v) { return v; }
+};
+template <> struct Traits<double> {
+  using Acc = double;
+  static __device__ __forceinline__ double to_acc(double v) { return v; }
+  static __device__ __forceinline__ double from_acc(double v) { return v; }
+};
+template <> struct Traits<__nv_bfloat16> {
+  using Acc = float;
+  static __device__ __forceinline__ float to_acc(__nv_bfloat16 v) { return __bfloat162float(v); }
+  static __device__ __forceinline__ __nv_bfloat16 from_acc(float v) { return __float2bfloat16_rn(v); }
+};
+template <> struct Traits<__half> {
+  using Acc = float;
+  static __device__ __forceinline__ float to_acc(__half v) { return __half2float(v); }
+  static __device__ __forceinline__ __half from_acc(float v) { return __float2half_rn(v); }
+};
+
+// exp2 in the accumulation type.  fp32 uses the MUFU ex2 (ex2.approx.ftz,
+// ~2 ulp); fp64 uses the libdevice exp2 (the reference's float64 accuracy).
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ double fast_exp2(double x) { return exp2(x); }
+__device__ __forceinline__ float acc_log(float x) { return logf(x); }
+__device__ __forceinline__ double acc_log(double x) { return log(x); }
+
+template <typename A> struct Lim;
+template <> struct Lim<float> {
+  static __device__ __forceinline__ float lowest() { return -3.402823466e38f; }
+  static __device__ __forceinline__ float ninf() { return -__int_as_float(0x7f800000); }
+  static constexpr float kLog2e = 1.4426950408889634f;
+};
+template <> struct Lim<double> {
+  static __device__ __forceinline__ double lowest() { return -1.7976931348623157e308; }
+  static __device__ __forceinline__ double ninf() { return -__longlong_as_double(0x7ff0000000000000ll); }
+  static constexpr double kLog2e = 1.4426950408889634074;
+};
+
+// ------------------------------------------------------------------ warp reductions
+template <typename A> __device__ __forceinline__ A warp_max(A v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+template <typename A> __device__ __forceinline__ A warp_sum(A v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Online (max, sum e^(x-max), sum e^(x-max)*x) triple, the row statistics of
+// log-softmax and entropy.  merge() is associative up to rounding; callers
+// merge in a fixed order so results are deterministic.
+template <typename A> struct RowStat {
+  A m, s, sx;
+  __device__ __forceinline__ void init() { m = Lim<A>::ninf(); s = A(0); sx = A(0); }
+  __device__ __forceinline__ void merge(A m2, A s2, A sx2) {
+    A mn = fmax(m, m2);
+    if (mn == Lim<A>::ninf()) return;  // both empty / all -inf
+    A a = fast_exp2((m - mn) * Lim<A>::kLog2e);
+    A b = fast_exp2((m2 - mn) * Lim<A>::kLog2e);
+    s = s * a + s2 * b;
+    sx = sx * a + sx2 * b;
+    m = mn;
+  }
+  __device__ __forceinline__ void warp_reduce() {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      A m2 = __shfl_xor_sync(0xffffffffu, m, o);
+      A s2 = __shfl_xor_sync(0xffffffffu, s, o);
+      A x2 = __shfl_xor_sync(0xffffffffu, sx, o);
+      merge(m2, s2, x2);
+    }
+  }
+};
+
+// ------------------------------------------------------------------ PTX: mbarrier / bulk copy / cluster
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init_cluster() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// acquire at cluster scope: pairs with remote release-arrives from peer CTAs.
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAITC_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 1-D bulk copy global -> shared, completion signalled on an mbarrier (TMA engine).
+__device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gsrc, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// 1-D bulk copy shared -> global (bulk-group completion).
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* smem_src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+               "r"(smem_u32(smem_src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N> __device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N> __device__ __forceinline__ void bulk_wait() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_id_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t nclusters_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_cluster_f64(uint32_t addr, double v) {
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
+}
+__device__ __forceinline__ void mbar_remote_arrive_release(uint32_t remote_bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote_bar)
+               : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+
+}  // namespace areal

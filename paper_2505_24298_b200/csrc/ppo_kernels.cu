@@ -1,0 +1,795 @@
+// ppo_kernels.cu — K1 (log-softmax-gather + entropy) and K2 (decoupled-PPO loss
+// fused with its backward into dlogits) for sm_100a.
+//
+// Reference semantics: /root/reference/pkg/src/asyncrl/trainer.py:150-195
+// (_surrogate_terms) and policy.py:145-163 (log_softmax, batch_token_log_probs),
+// restated on given logits; see DESIGN.md §3 for the data layout and rooflines.
+//
+// Two kernels per op:
+//   row_warp : one warp per row, any vocab / alignment; both passes read global
+//              memory (the second pass hits L1/L2).  Small-vocab and fallback path.
+//   row_ring : persistent, warp-specialised.  A producer thread streams the row
+//              through a ring of 16 KB shared-memory chunks with 1-D TMA bulk
+//              copies (cp.async.bulk + mbarrier complete_tx).  K2 keeps the whole
+//              row slice resident: pass 1 reduces (max, sum e^x, sum e^x*x) as
+//              chunks land, the CTAs of a thread-block cluster (which split the
+//              vocab) exchange their partials through DSMEM, pass 2 rewrites each
+//              chunk in place as dlogits and streams it out with a bulk store.
+//              HBM traffic = one logits read + one dlogits write per element.
+#include <type_traits>
+
+#include "common.cuh"
+
+namespace areal {
+
+// ------------------------------------------------------------------ arguments
+struct PpoArgs {
+  const char* logits;      // row r at logits + r*ld_in_bytes
+  char* dlogits;           // row r at dlogits + r*ld_out_bytes (BWD only)
+  int64_t ld_in_bytes, ld_out_bytes;
+  int64_t n_rows, vocab;
+  const int64_t* tokens;
+  const double* behav;
+  const double* prox;
+  const double* adv;
+  const int32_t* versions;
+  const int32_t* row_index;
+  double* lp_out;
+  double* ent_out;
+  double* stats;           // [8] accumulated (+=) by the last CTA
+  double* partials;        // workspace: [gridDim][8]
+  unsigned int* counter;   // workspace: ticket for the last-CTA reduction
+  double clip_eps, behav_cap, grad_scale;
+  int decoupled, eta_mask, cur_version;
+  // ring kernel geometry
+  int cluster_size;
+  int64_t slice16;         // 16-byte units per cluster rank
+  int nslots;
+};
+
+// ------------------------------------------------------------------ per-token epilogue (fp64)
+// trainer.py:165-195 for one token, exact IEEE op order (no FMA contraction):
+// scale/ratio, validity, clipped surrogate, take mask, coefficient, counters.
+struct TokenTerms {
+  double coef, obj, ratio;
+  bool valid, clipped, masked;
+};
+
+__device__ __forceinline__ TokenTerms ppo_token(double lp, double behav, double prox, double adv,
+                                                int version, const PpoArgs& a) {
+  TokenTerms t;
+  double scale, ratio;
+  if (a.decoupled) {
+    scale = exp(__dsub_rn(prox, behav));  // trainer.py:166
+    ratio = exp(__dsub_rn(lp, prox));     // trainer.py:167
+  } else {
+    scale = 1.0;                          // trainer.py:169
+    ratio = exp(__dsub_rn(lp, behav));    // trainer.py:170
+  }
+  const bool valid = isfinite(scale) && isfinite(ratio);  // trainer.py:172
+  bool masked = false;
+  if (a.eta_mask >= 0 && (a.cur_version - version) > a.eta_mask) masked = true;
+  if (a.behav_cap > 0.0 && valid && scale > a.behav_cap) masked = true;
+  const bool v = valid && !masked;
+  const double lo = __dsub_rn(1.0, a.clip_eps), hi = __dadd_rn(1.0, a.clip_eps);
+  const double P = __dmul_rn(ratio, adv);                          // trainer.py:173
+  const double Cl = __dmul_rn(fmin(fmax(ratio, lo), hi), adv);     // trainer.py:174
+  const double mn = (Cl < P) ? Cl : P;                             // np.minimum (NaN-propagating via P)
+  t.obj = v ? __dmul_rn(scale, mn) : 0.0;                          // trainer.py:175-176
+  const bool take = (P <= Cl) && v;                                // trainer.py:177
+  t.coef = take ? __dmul_rn(__dmul_rn(scale, adv), ratio) : 0.0;   // trainer.py:179
+  t.clipped = v && (Cl < P);                                       // trainer.py:186
+  t.ratio = ratio;
+  t.valid = v;
+  t.masked = masked;
+  return t;
+}
+
+__device__ __forceinline__ void stats_add(double st[AREAL_N_STATS], const TokenTerms& t,
+                                          double ent) {
+  st[AREAL_STAT_OBJECTIVE_SUM] += t.obj;
+  st[AREAL_STAT_N_VALID] += t.valid ? 1.0 : 0.0;
+  st[AREAL_STAT_N_CLIPPED] += t.clipped ? 1.0 : 0.0;
+  st[AREAL_STAT_RATIO_SUM] += t.valid ? t.ratio : 0.0;
+  st[AREAL_STAT_N_EXCLUDED] += t.valid ? 0.0 : 1.0;
+  st[AREAL_STAT_N_MASKED] += t.masked ? 1.0 : 0.0;
+  st[AREAL_STAT_ENTROPY_SUM] += t.valid ? ent : 0.0;
+  st[AREAL_STAT_N_TOKENS] += 1.0;
+}
+
+// Deterministic grid reduction of per-CTA stats: every CTA writes its partial,
+// the last CTA to finish (atomic ticket) sums them in CTA order and adds the
+// result into a.stats, then re-arms the ticket.  Call with all CTA threads.
+__device__ void finalize_stats(const PpoArgs& a, const double cta_stats[AREAL_N_STATS],
+                               int nthreads) {
+  __shared__ unsigned int s_last;
+  if (threadIdx.x == 0) {
+    double* p = a.partials + (size_t)blockIdx.x * AREAL_N_STATS;
+#pragma unroll
+    for (int j = 0; j < AREAL_N_STATS; ++j) p[j] = cta_stats[j];
+    __threadfence();
+    unsigned int ticket = atomicAdd(a.counter, 1u);
+    s_last = (ticket == gridDim.x - 1) ? 1u : 0u;
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    if (threadIdx.x < AREAL_N_STATS) {
+      const volatile double* p = a.partials;
+      double acc = 0.0;
+      for (unsigned int b = 0; b < gridDim.x; ++b) acc += p[(size_t)b * AREAL_N_STATS + threadIdx.x];
+      a.stats[threadIdx.x] += acc;
+    }
+    if (threadIdx.x == 0) *a.counter = 0u;
+  }
+  (void)nthreads;
+}
+
+// ------------------------------------------------------------------ exponent helpers
+// fp32 path works in the log2 domain with the MUFU ex2; fp64 uses libdevice exp.
+template <typename A> struct Ex;
+template <> struct Ex<float> {
+  // shift constant for a running max m
+  static __device__ __forceinline__ float shift(float m) { return m * Lim<float>::kLog2e; }
+  static __device__ __forceinline__ float e(float x, float c) {
+    return fast_exp2(fmaf(x, Lim<float>::kLog2e, -c));
+  }
+  // lse in "shift units" (log2 domain) from (m, s)
+  static __device__ __forceinline__ float lse_shift(float m, float s) {
+    return m * Lim<float>::kLog2e + __log2f(s);
+  }
+  static __device__ __forceinline__ double lse_nat(float lse2) {
+    return (double)lse2 * 0.69314718055994530942;
+  }
+};
+template <> struct Ex<double> {
+  static __device__ __forceinline__ double shift(double m) { return m; }
+  static __device__ __forceinline__ double e(double x, double c) { return exp(x - c); }
+  static __device__ __forceinline__ double lse_shift(double m, double s) { return m + log(s); }
+  static __device__ __forceinline__ double lse_nat(double l) { return l; }
+};
+
+// Fold a batch of values (already max-reduced into lmax) into a running RowStat.
+template <typename A, int N>
+__device__ __forceinline__ void fold(RowStat<A>& rs, const A (&v)[N], A lmax) {
+  const A mn = fmax(rs.m, lmax);
+  const A muse = (mn == Lim<A>::ninf()) ? A(0) : mn;
+  const A c = Ex<A>::shift(muse);
+  const A r = Ex<A>::e(rs.m, c);  // rescale of the old partial sums (0 when m = -inf)
+  A s = rs.s * r, sx = rs.sx * r;
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    const A e = Ex<A>::e(v[i], c);
+    s += e;
+    sx += e * fmax(v[i], Lim<A>::lowest());  // 0 * (-inf) guarded: p log p := 0
+  }
+  rs.m = mn;
+  rs.s = s;
+  rs.sx = sx;
+}
+
+// ------------------------------------------------------------------ 16-byte vector (un)packing
+template <typename T> struct Vec;
+template <> struct Vec<__nv_bfloat16> {
+  static constexpr int N = 8;
+  static __device__ __forceinline__ void unpack(const uint4& q, float (&o)[8]) {
+    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      o[2 * i] = __uint_as_float(w[i] << 16);
+      o[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+    }
+  }
+  static __device__ __forceinline__ uint4 pack(const float (&o)[8]) {
+    uint32_t w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      __nv_bfloat162 h = __floats2bfloat162_rn(o[2 * i], o[2 * i + 1]);
+      w[i] = *reinterpret_cast<uint32_t*>(&h);
+    }
+    return make_uint4(w[0], w[1], w[2], w[3]);
+  }
+};
+template <> struct Vec<__half> {
+  static constexpr int N = 8;
+  static __device__ __forceinline__ void unpack(const uint4& q, float (&o)[8]) {
+    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      __half2 h = *reinterpret_cast<const __half2*>(&w[i]);
+      float2 f = __half22float2(h);
+      o[2 * i] = f.x;
+      o[2 * i + 1] = f.y;
+    }
+  }
+  static __device__ __forceinline__ uint4 pack(const float (&o)[8]) {
+    uint32_t w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      __half2 h = __floats2half2_rn(o[2 * i], o[2 * i + 1]);
+      w[i] = *reinterpret_cast<uint32_t*>(&h);
+    }
+    return make_uint4(w[0], w[1], w[2], w[3]);
+  }
+};
+template <> struct Vec<float> {
+  static constexpr int N = 4;
+  static __device__ __forceinline__ void unpack(const uint4& q, float (&o)[4]) {
+    o[0] = __uint_as_float(q.x);
+    o[1] = __uint_as_float(q.y);
+    o[2] = __uint_as_float(q.z);
+    o[3] = __uint_as_float(q.w);
+  }
+  static __device__ __forceinline__ uint4 pack(const float (&o)[4]) {
+    return make_uint4(__float_as_uint(o[0]), __float_as_uint(o[1]), __float_as_uint(o[2]),
+                      __float_as_uint(o[3]));
+  }
+};
+template <> struct Vec<double> {
+  static constexpr int N = 2;
+  static __device__ __forceinline__ void unpack(const uint4& q, double (&o)[2]) {
+    o[0] = __hiloint2double((int)q.y, (int)q.x);
+    o[1] = __hiloint2double((int)q.w, (int)q.z);
+  }
+  static __device__ __forceinline__ uint4 pack(const double (&o)[2]) {
+    const long long a = __double_as_longlong(o[0]), b = __double_as_longlong(o[1]);
+    return make_uint4((uint32_t)a, (uint32_t)(a >> 32), (uint32_t)b, (uint32_t)(b >> 32));
+  }
+};
+
+// ------------------------------------------------------------------ shared per-row token prologue
+template <typename T>
+__device__ __forceinline__ double token_logit(const PpoArgs& a, const T* row, int64_t tok) {
+  if (tok < 0 || tok >= a.vocab) return __longlong_as_double(0x7ff8000000000000ll);  // NaN: excluded
+  return (double)Traits<T>::to_acc(row[tok]);
+}
+
+// ================================================================== row_warp kernel
+constexpr int kWarpKernelWarps = 8;
+constexpr int kWarpUnroll = 8;
+
+template <typename T, bool BWD>
+__device__ __forceinline__ void row_warp_body(const PpoArgs& a) {
+  using A = typename Traits<T>::Acc;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t nw = (int64_t)gridDim.x * kWarpKernelWarps;
+  double st[AREAL_N_STATS];
+#pragma unroll
+  for (int j = 0; j < AREAL_N_STATS; ++j) st[j] = 0.0;
+  const int64_t V = a.vocab;
+
+  for (int64_t row = (int64_t)blockIdx.x * kWarpKernelWarps + warp; row < a.n_rows; row += nw) {
+    const T* x = reinterpret_cast<const T*>(a.logits + row * a.ld_in_bytes);
+    const int64_t idx = a.row_index ? (int64_t)a.row_index[row] : row;
+    const int64_t tok = a.tokens[idx];
+    RowStat<A> rs;
+    rs.init();
+    for (int64_t base = 0; base < V; base += 32 * kWarpUnroll) {
+      A v[kWarpUnroll];
+      A lmax = Lim<A>::ninf();
+#pragma unroll
+      for (int u = 0; u < kWarpUnroll; ++u) {
+        const int64_t i = base + u * 32 + lane;
+        v[u] = (i < V) ? Traits<T>::to_acc(x[i]) : Lim<A>::ninf();
+        lmax = fmax(lmax, v[u]);
+      }
+      fold(rs, v, lmax);
+    }
+    rs.warp_reduce();
+    const A lse_s = Ex<A>::lse_shift(rs.m == Lim<A>::ninf() ? A(0) : rs.m, rs.s);
+    const double lse = Ex<A>::lse_nat(lse_s);
+    const double ent = lse - (double)(rs.sx / rs.s);
+    double gc = 0.0;
+    if (lane == 0) {
+      const double lp = token_logit<T>(a, x, tok) - lse;
+      if (a.lp_out) a.lp_out[idx] = lp;
+      if (a.ent_out) a.ent_out[idx] = ent;
+      if (BWD) {
+        const TokenTerms t = ppo_token(lp, a.behav[idx], a.prox ? a.prox[idx] : 0.0, a.adv[idx],
+                                       a.versions ? a.versions[idx] : 0, a);
+        stats_add(st, t, ent);
+        gc = a.grad_scale * t.coef;
+      }
+    }
+    if (BWD) {
+      gc = __shfl_sync(0xffffffffu, gc, 0);
+      const A g = (A)gc;
+      T* d = reinterpret_cast<T*>(a.dlogits + row * a.ld_out_bytes);
+      for (int64_t i = lane; i < V; i += 32) {
+        const A xv = Traits<T>::to_acc(x[i]);
+        A p;
+        if constexpr (std::is_same<A, float>::value)
+          p = fast_exp2(fmaf(xv, Lim<float>::kLog2e, -lse_s));
+        else
+          p = exp(xv - lse_s);
+        d[i] = Traits<T>::from_acc(g * (p - (i == tok ? A(1) : A(0))));
+      }
+    }
+  }
+  if (BWD) {
+    // block reduce in warp order, then deterministic grid finalize
+    __shared__ double red[kWarpKernelWarps][AREAL_N_STATS];
+    if (lane == 0)
+      for (int j = 0; j < AREAL_N_STATS; ++j) red[warp][j] = st[j];
+    __syncthreads();
+    double cta[AREAL_N_STATS];
+    for (int j = 0; j < AREAL_N_STATS; ++j) {
+      double acc = 0.0;
+      for (int w = 0; w < kWarpKernelWarps; ++w) acc += red[w][j];
+      cta[j] = acc;
+    }
+    finalize_stats(a, cta, kWarpKernelWarps * 32);
+  }
+}
+
+// ================================================================== row_ring kernel
+constexpr int kChunkBytes = 16384;
+constexpr int kConsumerWarps = 8;
+constexpr int kConsumers = kConsumerWarps * 32;
+constexpr int kRingThreads = kConsumers + 32;  // + 1 producer warp
+constexpr int kBarConsumers = 1;                // named barrier id among consumer warps
+
+struct RingSmemTail {
+  uint64_t xbar[2];           // DSMEM exchange barriers (double-buffered by row parity)
+  double xval[2][8][3];       // [parity][rank][m, s, sx]
+  double red[kConsumerWarps][3];
+  double bc_gc;               // broadcast: grad_scale * coef
+  double bc_lse;              // broadcast: lse in shift units
+};
+
+template <typename T, bool BWD>
+__device__ __forceinline__ void row_ring_body(const PpoArgs& a) {
+  using A = typename Traits<T>::Acc;
+  constexpr int E = Vec<T>::N;                 // elements per 16 bytes
+  extern __shared__ __align__(1024) unsigned char smem[];
+  const int nslots = a.nslots;
+  unsigned char* ring = smem;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)nslots * kChunkBytes);
+  uint64_t* empty = full + nslots;
+  RingSmemTail* tail = reinterpret_cast<RingSmemTail*>(empty + nslots);
+
+  const int CS = a.cluster_size;
+  const uint32_t rank = CS > 1 ? cluster_ctarank() : 0u;
+  const int64_t cid = CS > 1 ? (int64_t)cluster_id_x() : (int64_t)blockIdx.x;
+  const int64_t ncl = CS > 1 ? (int64_t)nclusters_x() : (int64_t)gridDim.x;
+  const int64_t V16 = (a.vocab * (int64_t)sizeof(T)) / 16;
+  const int64_t b16 = (int64_t)rank * a.slice16;
+  const int64_t e16 = min(V16, b16 + a.slice16);
+  const int64_t slice_bytes = e16 > b16 ? (e16 - b16) * 16 : 0;
+  const int nchunks = (int)((slice_bytes + kChunkBytes - 1) / kChunkBytes);
+  const int64_t slice_e0 = b16 * E;  // first vocab element of this rank's slice
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < nslots; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], BWD ? 1 : kConsumerWarps);
+    }
+    mbar_init(&tail->xbar[0], CS);
+    mbar_init(&tail->xbar[1], CS);
+    fence_mbar_init_cluster();
+  }
+  __syncthreads();
+  if (CS > 1) cluster_sync_all();  // peers' exchange barriers initialised before any remote arrive
+
+  const int tid = threadIdx.x;
+  double st[AREAL_N_STATS];
+#pragma unroll
+  for (int j = 0; j < AREAL_N_STATS; ++j) st[j] = 0.0;
+
+  if (tid >= kConsumers) {
+    // ---------------- producer warp: one elected lane issues the TMA bulk loads
+    if (tid == kConsumers) {
+      uint32_t k = 0;
+      for (int64_t row = cid; row < a.n_rows; row += ncl) {
+        const char* src = a.logits + row * a.ld_in_bytes + b16 * 16;
+        for (int c = 0; c < nchunks; ++c, ++k) {
+          const uint32_t slot = k % nslots, round = k / nslots;
+          if (round > 0) mbar_wait(&empty[slot], (round - 1) & 1);
+          const uint32_t bytes = (uint32_t)min((int64_t)kChunkBytes, slice_bytes - (int64_t)c * kChunkBytes);
+          mbar_arrive_expect_tx(&full[slot], bytes);
+          bulk_g2s(ring + (size_t)slot * kChunkBytes, src + (size_t)c * kChunkBytes, bytes, &full[slot]);
+        }
+      }
+    }
+  } else {
+    // ---------------- consumer warps
+    const int warp = tid >> 5, lane = tid & 31;
+    uint32_t k = 0;        // ring position of this row's first chunk
+    uint32_t pending = 0;  // BWD: stores issued whose slot is not yet released (thread 0)
+    uint32_t pend_k = 0;
+    int it = 0;
+    for (int64_t row = cid; row < a.n_rows; row += ncl, ++it) {
+      const T* xrow = reinterpret_cast<const T*>(a.logits + row * a.ld_in_bytes);
+      const int64_t idx = a.row_index ? (int64_t)a.row_index[row] : row;
+      int64_t tok = 0;
+      double xa = 0.0;
+      if (tid == 0) {
+        tok = a.tokens[idx];
+        xa = token_logit<T>(a, xrow, tok);
+      }
+      // ---- pass 1: online (max, sum, sum*x) over the resident chunks
+      RowStat<A> rs;
+      rs.init();
+      for (int c = 0; c < nchunks; ++c) {
+        const uint32_t kk = k + c, slot = kk % nslots, round = kk / nslots;
+        mbar_wait(&full[slot], round & 1);
+        const int nvec = (int)(min((int64_t)kChunkBytes, slice_bytes - (int64_t)c * kChunkBytes) / 16);
+        const uint4* q = reinterpret_cast<const uint4*>(ring + (size_t)slot * kChunkBytes);
+        constexpr int kPer = kChunkBytes / 16 / kConsumers;  // vectors per thread per full chunk
+        A v[kPer * E];
+        A lmax = Lim<A>::ninf();
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) {
+          const int vi = tid + j * kConsumers;
+          A f[E];
+          if (vi < nvec) {
+            Vec<T>::unpack(q[vi], f);
+          } else {
+#pragma unroll
+            for (int e = 0; e < E; ++e) f[e] = Lim<A>::ninf();
+          }
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            v[j * E + e] = f[e];
+            lmax = fmax(lmax, f[e]);
+          }
+        }
+        fold(rs, v, lmax);
+        if (!BWD) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[slot]);
+        }
+      }
+      // ---- CTA reduce (fixed order)
+      rs.warp_reduce();
+      if (lane == 0) {
+        tail->red[warp][0] = (double)rs.m;
+        tail->red[warp][1] = (double)rs.s;
+        tail->red[warp][2] = (double)rs.sx;
+      }
+      named_bar_sync(kBarConsumers, kConsumers);
+      if (tid == 0) {
+        RowStat<A> cta;
+        cta.init();
+        for (int w = 0; w < kConsumerWarps; ++w)
+          cta.merge((A)tail->red[w][0], (A)tail->red[w][1], (A)tail->red[w][2]);
+        RowStat<A> tot = cta;
+        if (CS > 1) {
+          // ---- cluster exchange through DSMEM: write my partial into every
+          // rank's slot [parity][my rank], release-arrive on its barrier.
+          const int par = it & 1;
+          for (int r = 0; r < CS; ++r) {
+            const uint32_t base = mapa_shared(smem_u32(&tail->xval[par][rank][0]), (uint32_t)r);
+            st_cluster_f64(base, (double)cta.m);
+            st_cluster_f64(base + 8, (double)cta.s);
+            st_cluster_f64(base + 16, (double)cta.sx);
+            mbar_remote_arrive_release(mapa_shared(smem_u32(&tail->xbar[par]), (uint32_t)r));
+          }
+          mbar_wait_cluster(&tail->xbar[par], (it >> 1) & 1);
+          tot.init();
+          for (int r = 0; r < CS; ++r)
+            tot.merge((A)tail->xval[par][r][0], (A)tail->xval[par][r][1], (A)tail->xval[par][r][2]);
+        }
+        const A lse_s = Ex<A>::lse_shift(tot.m == Lim<A>::ninf() ? A(0) : tot.m, tot.s);
+        const double lse = Ex<A>::lse_nat(lse_s);
+        const double ent = lse - (double)(tot.sx / tot.s);
+        const double lp = xa - lse;
+        double gc = 0.0;
+        if (rank == 0) {
+          if (a.lp_out) a.lp_out[idx] = lp;
+          if (a.ent_out) a.ent_out[idx] = ent;
+        }
+        if (BWD) {
+          const TokenTerms t = ppo_token(lp, a.behav[idx], a.prox ? a.prox[idx] : 0.0, a.adv[idx],
+                                         a.versions ? a.versions[idx] : 0, a);
+          if (rank == 0) stats_add(st, t, ent);
+          gc = a.grad_scale * t.coef;
+        }
+        tail->bc_gc = gc;
+        tail->bc_lse = (double)lse_s;
+        tail->red[0][0] = __longlong_as_double(tok);  // token id broadcast
+      }
+      if (BWD) {
+        named_bar_sync(kBarConsumers, kConsumers);
+        const A g = (A)tail->bc_gc;
+        const A lse_s = (A)tail->bc_lse;
+        const int64_t tok_local = __double_as_longlong(tail->red[0][0]) - slice_e0;
+        char* drow = a.dlogits + row * a.ld_out_bytes + b16 * 16;
+        // ---- pass 2: dlogits in place, then bulk store
+        for (int c = 0; c < nchunks; ++c) {
+          const uint32_t kk = k + c, slot = kk % nslots;
+          const int cbytes = (int)min((int64_t)kChunkBytes, slice_bytes - (int64_t)c * kChunkBytes);
+          const int nvec = cbytes / 16;
+          uint4* q = reinterpret_cast<uint4*>(ring + (size_t)slot * kChunkBytes);
+          constexpr int kPer = kChunkBytes / 16 / kConsumers;
+#pragma unroll
+          for (int j = 0; j < kPer; ++j) {
+            const int vi = tid + j * kConsumers;
+            if (vi < nvec) {
+              A f[E];
+              Vec<T>::unpack(q[vi], f);
+              const int64_t e0 = (int64_t)c * (kChunkBytes / sizeof(T)) + (int64_t)vi * E;
+#pragma unroll
+              for (int e = 0; e < E; ++e) {
+                A p;
+                if constexpr (std::is_same<A, float>::value)
+                  p = fast_exp2(fmaf(f[e], Lim<float>::kLog2e, -lse_s));
+                else
+                  p = exp(f[e] - lse_s);
+                f[e] = g * (p - ((e0 + e) == tok_local ? A(1) : A(0)));
+              }
+              q[vi] = Vec<T>::pack(f);
+            }
+          }
+          fence_proxy_async_smem();
+          named_bar_sync(kBarConsumers, kConsumers);
+          if (tid == 0) {
+            bulk_s2g(drow + (size_t)c * kChunkBytes, ring + (size_t)slot * kChunkBytes, (uint32_t)cbytes);
+            bulk_commit();
+            if (pending) {
+              // the previous store must have finished reading its slot before reuse
+              bulk_wait_read<1>();
+              mbar_arrive(&empty[pend_k % nslots]);
+            }
+            pending = 1;
+            pend_k = kk;
+          }
+        }
+      } else {
+        named_bar_sync(kBarConsumers, kConsumers);  // protect tail->red reuse across rows
+      }
+      k += nchunks;
+    }
+    if (BWD && tid == 0) {
+      bulk_wait<0>();  // all dlogits stores complete before the CTA retires
+      if (pending) mbar_arrive(&empty[pend_k % nslots]);
+    }
+  }
+  // all threads: final stats reduction (rank-0 CTAs carry the counters)
+  __syncthreads();
+  if (BWD) {
+    double cta[AREAL_N_STATS];
+    __shared__ double s_st[AREAL_N_STATS];
+    if (tid == 0)
+      for (int j = 0; j < AREAL_N_STATS; ++j) s_st[j] = st[j];
+    __syncthreads();
+    for (int j = 0; j < AREAL_N_STATS; ++j) cta[j] = s_st[j];
+    finalize_stats(a, cta, kRingThreads);
+  }
+  if (CS > 1) cluster_sync_all();  // no CTA exits while a peer may still address its smem
+}
+
+// Distinct entry points per op so profiles name them: K1 = logprob_*, K2 = ppo_*.
+template <typename T>
+__global__ void __launch_bounds__(kWarpKernelWarps * 32) logprob_warp_kernel(PpoArgs a) {
+  row_warp_body<T, false>(a);
+}
+template <typename T>
+__global__ void __launch_bounds__(kWarpKernelWarps * 32) ppo_warp_kernel(PpoArgs a) {
+  row_warp_body<T, true>(a);
+}
+template <typename T>
+__global__ void __launch_bounds__(kRingThreads, 1) logprob_ring_kernel(PpoArgs a) {
+  row_ring_body<T, false>(a);
+}
+template <typename T>
+__global__ void __launch_bounds__(kRingThreads, 1) ppo_ring_kernel(PpoArgs a) {
+  row_ring_body<T, true>(a);
+}
+
+// ================================================================== host side
+static size_t ring_smem_bytes(int nslots) {
+  return (size_t)nslots * kChunkBytes + 2 * (size_t)nslots * sizeof(uint64_t) + sizeof(RingSmemTail);
+}
+
+struct DevInfo {
+  int dev = -1, sms = 0, smem_optin = 0;
+};
+static DevInfo get_dev() {
+  static thread_local DevInfo cache[16];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  DevInfo& d = cache[dev & 15];
+  if (d.dev != dev) {
+    d.dev = dev;
+    cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&d.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  }
+  return d;
+}
+
+static int max_slots(const DevInfo& d) {
+  int n = 16;
+  while (n > 2 && ring_smem_bytes(n) > (size_t)d.smem_optin) --n;
+  return n;
+}
+
+template <typename T, bool BWD>
+static int launch_ring(PpoArgs a, cudaStream_t stream, int cs_force) {
+  DevInfo d = get_dev();
+  const int nslots = max_slots(d);
+  const int64_t V16 = (a.vocab * (int64_t)sizeof(T)) / 16;
+  int CS = 1;
+  if (BWD) {
+    // smallest cluster whose slice fits the ring with one slot of slack
+    const int cands[4] = {1, 2, 4, 8};
+    CS = -1;
+    for (int ci = 0; ci < 4; ++ci) {
+      const int64_t sl = (V16 + cands[ci] - 1) / cands[ci];
+      const int64_t nch = (sl * 16 + kChunkBytes - 1) / kChunkBytes;
+      if (nch <= nslots - 1) {
+        CS = cands[ci];
+        break;
+      }
+    }
+    if (CS < 0) return AREAL_ERR_UNSUPPORTED;
+    if (cs_force > 0) CS = cs_force;
+  }
+  a.cluster_size = CS;
+  a.slice16 = (V16 + CS - 1) / CS;
+  a.nslots = nslots;
+  const size_t smem = ring_smem_bytes(nslots);
+  auto kern = BWD ? ppo_ring_kernel<T> : logprob_ring_kernel<T>;
+  static thread_local int attr_set[16] = {0};
+  int dev = d.dev & 15;
+  if (!(attr_set[dev] & 1)) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return AREAL_ERR_CUDA;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+      cudaGetLastError();
+    attr_set[dev] |= 1;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  cfg.blockDim = dim3(kRingThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int max_clusters = d.sms / CS;
+  if (CS > 1) {
+    cfg.gridDim = dim3(CS);
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) == cudaSuccess && n > 0) max_clusters = n;
+    else cudaGetLastError();
+  }
+  const int64_t ncl = std::min<int64_t>(a.n_rows, (int64_t)max_clusters);
+  cfg.gridDim = dim3((unsigned)(ncl * CS));
+  if (cudaLaunchKernelEx(&cfg, kern, a) != cudaSuccess) return AREAL_ERR_CUDA;
+  return AREAL_OK;
+}
+
+template <typename T, bool BWD>
+static int launch_warp(PpoArgs a, cudaStream_t stream) {
+  DevInfo d = get_dev();
+  const int64_t blocks_needed = (a.n_rows + kWarpKernelWarps - 1) / kWarpKernelWarps;
+  const int64_t grid = std::min<int64_t>(blocks_needed, (int64_t)d.sms * 8);
+  auto kern = BWD ? ppo_warp_kernel<T> : logprob_warp_kernel<T>;
+  kern<<<(unsigned)grid, kWarpKernelWarps * 32, 0, stream>>>(a);
+  AREAL_CUDA_CHECK_LAUNCH();
+  return AREAL_OK;
+}
+
+static int dtype_size(int dtype) {
+  switch (dtype) {
+    case AREAL_F32: return 4;
+    case AREAL_BF16: return 2;
+    case AREAL_F16: return 2;
+    case AREAL_F64: return 8;
+    default: return 0;
+  }
+}
+
+// AUTO: ring when rows are >= 16 KB and every row start is 16-byte aligned.
+static bool ring_ok(const void* base, int64_t ld_bytes, int64_t vocab, int es) {
+  return ((uintptr_t)base % 16 == 0) && (ld_bytes % 16 == 0) && ((vocab * es) % 16 == 0);
+}
+
+template <bool BWD>
+static int dispatch(PpoArgs a, int dtype, int algo, cudaStream_t stream) {
+  const int es = dtype_size(dtype);
+  bool ring = false;
+  const bool aligned = ring_ok(a.logits, a.ld_in_bytes, a.vocab, es) &&
+                       (!BWD || ring_ok(a.dlogits, a.ld_out_bytes, a.vocab, es));
+  if (algo == AREAL_ALGO_ROW_RING) {
+    if (!aligned) return AREAL_ERR_MISALIGNED;
+    ring = true;
+  } else if (algo == AREAL_ALGO_AUTO) {
+    ring = aligned && a.vocab * es >= 16384;
+  }
+  if (ring) {
+    int rc;
+    switch (dtype) {
+      case AREAL_F32: rc = launch_ring<float, BWD>(a, stream, 0); break;
+      case AREAL_BF16: rc = launch_ring<__nv_bfloat16, BWD>(a, stream, 0); break;
+      case AREAL_F16: rc = launch_ring<__half, BWD>(a, stream, 0); break;
+      case AREAL_F64: rc = launch_ring<double, BWD>(a, stream, 0); break;
+      default: return AREAL_ERR_BAD_DTYPE;
+    }
+    if (rc != AREAL_ERR_UNSUPPORTED || algo == AREAL_ALGO_ROW_RING) return rc;
+  }
+  switch (dtype) {
+    case AREAL_F32: return launch_warp<float, BWD>(a, stream);
+    case AREAL_BF16: return launch_warp<__nv_bfloat16, BWD>(a, stream);
+    case AREAL_F16: return launch_warp<__half, BWD>(a, stream);
+    case AREAL_F64: return launch_warp<double, BWD>(a, stream);
+    default: return AREAL_ERR_BAD_DTYPE;
+  }
+}
+
+static constexpr size_t kCounterBytes = 256;
+
+}  // namespace areal
+
+using namespace areal;
+
+extern "C" int areal_logprob_fwd(const void* logits, int64_t ld_logits, int dtype, int64_t n_rows,
+                                 int64_t vocab, const int64_t* tokens, const int32_t* row_index,
+                                 double* lp_out, double* entropy_out, int algo, void* workspace,
+                                 size_t workspace_bytes, void* stream) {
+  const int es = dtype_size(dtype);
+  if (es == 0) return AREAL_ERR_BAD_DTYPE;
+  if (n_rows < 0 || vocab < 1 || ld_logits < vocab) return AREAL_ERR_BAD_SHAPE;
+  if (n_rows == 0) return AREAL_OK;
+  if (!logits || !tokens || (!lp_out && !entropy_out)) return AREAL_ERR_INVALID_ARGUMENT;
+  (void)workspace;
+  (void)workspace_bytes;
+  PpoArgs a = {};
+  a.logits = static_cast<const char*>(logits);
+  a.ld_in_bytes = ld_logits * es;
+  a.n_rows = n_rows;
+  a.vocab = vocab;
+  a.tokens = tokens;
+  a.row_index = row_index;
+  a.lp_out = lp_out;
+  a.ent_out = entropy_out;
+  return dispatch<false>(a, dtype, algo, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int areal_ppo_fwd_bwd(const void* logits, int64_t ld_logits, void* dlogits,
+                                 int64_t ld_dlogits, int dtype, int64_t n_rows, int64_t vocab,
+                                 const int64_t* tokens, const double* behav, const double* prox,
+                                 const double* adv, const int32_t* versions,
+                                 const int32_t* row_index, const areal_ppo_params_t* params,
+                                 double* lp_out, double* entropy_out, double* stats,
+                                 void* workspace, size_t workspace_bytes, void* stream) {
+  const int es = dtype_size(dtype);
+  if (es == 0) return AREAL_ERR_BAD_DTYPE;
+  if (!params) return AREAL_ERR_INVALID_ARGUMENT;
+  if (!(params->clip_eps > 0.0 && params->clip_eps < 1.0)) return AREAL_ERR_BAD_CLIP_EPS;
+  if (n_rows < 0 || vocab < 1 || ld_logits < vocab || ld_dlogits < vocab) return AREAL_ERR_BAD_SHAPE;
+  if (n_rows == 0) return AREAL_OK;
+  if (!logits || !dlogits || !tokens || !behav || !adv || !stats) return AREAL_ERR_INVALID_ARGUMENT;
+  if (params->decoupled && !prox) return AREAL_ERR_INVALID_ARGUMENT;
+  if (params->eta_mask >= 0 && !versions) return AREAL_ERR_INVALID_ARGUMENT;
+  if (!workspace || workspace_bytes < AREAL_WORKSPACE_BYTES) return AREAL_ERR_WORKSPACE;
+  PpoArgs a = {};
+  a.logits = static_cast<const char*>(logits);
+  a.dlogits = static_cast<char*>(dlogits);
+  a.ld_in_bytes = ld_logits * es;
+  a.ld_out_bytes = ld_dlogits * es;
+  a.n_rows = n_rows;
+  a.vocab = vocab;
+  a.tokens = tokens;
+  a.behav = behav;
+  a.prox = prox;
+  a.adv = adv;
+  a.versions = versions;
+  a.row_index = row_index;
+  a.lp_out = lp_out;
+  a.ent_out = entropy_out;
+  a.stats = stats;
+  a.counter = static_cast<unsigned int*>(workspace);
+  a.partials = reinterpret_cast<double*>(static_cast<char*>(workspace) + kCounterBytes);
+  a.clip_eps = params->clip_eps;
+  a.behav_cap = params->behav_weight_cap;
+  a.grad_scale = params->grad_scale;
+  a.decoupled = params->decoupled;
+  a.eta_mask = params->eta_mask;
+  a.cur_version = params->current_version;
+  return dispatch<true>(a, dtype, params->algo, static_cast<cudaStream_t>(stream));
+}

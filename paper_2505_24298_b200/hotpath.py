@@ -1,0 +1,298 @@
+"""LM-scale decoupled-PPO hot path: packed rollouts -> advantages -> prox log-probs
+-> micro-batch allocation/packing -> fused loss+backward, with data parallelism.
+
+This is ``asyncrl.trainer.train_step`` (trainer.py:285-346) restated for a real
+language model whose logits live on the GPU: the model is abstracted as two
+callbacks, so this module owns exactly the hot path and nothing else.
+
+    logits_fn(phase, minibatch, micro, rows) -> logits [len(rows), V] (CUDA)
+        phase 'prox'  : forward under the params at batch arrival (K1 consumes it)
+        phase 'train' : forward under the current params (K2 consumes it)
+        rows          : int32 CUDA tensor, global token index of each packed row
+    backward_fn(minibatch, micro, dlogits)   -> model backward from dlogits (optional)
+    update_fn(minibatch, stats)              -> optimizer step; stats is the
+        all-reduced float64[8] device tensor of the minibatch, so the caller
+        scales its accumulated gradients by 1 / max(stats[1], 1) (trainer.py:329-330)
+
+Data parallelism: every rank computes the same plan (K4 is
+deterministic, so no broadcast), the micro-batches of each minibatch are dealt
+to ranks longest-processing-time first by token count, and the only collective
+is one NCCL all-reduce of the 8 statistics per minibatch.
+"""
+from __future__ import annotations
+
+import heapq
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import kernels as K
+from .trainer import BatchError, minibatch_items, _status_error
+
+ADV_NORM_ALIASES = {"group": "group_token"}
+
+
+@dataclass(frozen=True)
+class HotPathConfig:
+    """TrainerConfig (trainer.py:38-53) fields that the hot path reads, + extensions."""
+    clip_eps: float = 0.2
+    minibatches: int = 4
+    micro_token_budget: int = 32768
+    micro_min_groups: int = 1
+    objective: str = "decoupled"
+    eta_mask: int = -1
+    behav_weight_cap: float = 0.0
+    adv_mode: str = "reference"
+    gamma: float = 1.0
+    lam: float = 1.0
+    adv_norm: str = "global"
+    adv_eps: float = 0.0
+    algo: str = "auto"
+
+    def __post_init__(self):
+        if not (0 < self.clip_eps < 1):
+            raise BatchError("clip_eps must be in (0, 1)")
+        if self.minibatches < 1:
+            raise BatchError("minibatches must be >= 1")
+        if self.micro_min_groups < 1:
+            raise BatchError("min_groups must be >= 1")
+        if self.objective not in ("decoupled", "naive"):
+            raise BatchError(f"unknown objective {self.objective!r}")
+
+
+@dataclass
+class PackedRollouts:
+    """One global batch in formation order (controller.form_batch order), on device.
+
+    traj_bounds is cu_seqlens (trainer.py:56-80 ``traj_bounds``); per-token
+    arrays are indexed by global token; group_ids (GRPO) by trajectory.
+    """
+    traj_bounds: torch.Tensor
+    traj_bounds_host: np.ndarray
+    tokens: torch.Tensor
+    behav: torch.Tensor
+    rewards: torch.Tensor
+    versions: torch.Tensor | None = None
+    group_ids: torch.Tensor | None = None
+    values: torch.Tensor | None = None
+
+    @property
+    def n_tokens(self) -> int:
+        return int(self.traj_bounds_host[-1])
+
+    @property
+    def n_traj(self) -> int:
+        return len(self.traj_bounds_host) - 1
+
+    def h2d_bytes(self) -> int:
+        ts = [self.traj_bounds, self.tokens, self.behav, self.rewards, self.versions,
+              self.group_ids, self.values]
+        return int(sum(t.numel() * t.element_size() for t in ts if t is not None))
+
+    @staticmethod
+    def from_host(traj_bounds, tokens, behav, rewards, versions=None, group_ids=None, values=None,
+                  device=None, non_blocking=True):
+        """Host (ideally pinned) arrays/tensors -> device copies on the current stream."""
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None else device
+
+        def up(x, dtype):
+            if x is None:
+                return None
+            t = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x))
+            return t.to(dtype).to(dev, non_blocking=non_blocking)
+
+        bh = np.asarray(traj_bounds.numpy() if isinstance(traj_bounds, torch.Tensor)
+                        else traj_bounds, dtype=np.int64)
+        return PackedRollouts(up(traj_bounds, torch.int64), bh, up(tokens, torch.int64),
+                              up(behav, torch.float64), up(rewards, torch.float64),
+                              up(versions, torch.int32), up(group_ids, torch.int32),
+                              up(values, torch.float64))
+
+
+@dataclass
+class StepPlan:
+    """Output of K4/K5 for one global batch plus this rank's share."""
+    items: list                 # non-empty trajectory ids per minibatch
+    device_plan: K.DevicePlan
+    gather: torch.Tensor        # int32 [n_packed]: packed position -> global token
+    group_cu: np.ndarray        # host copy of micro-batch token boundaries
+    n_groups: np.ndarray        # host, per minibatch
+    micro: list = field(default_factory=list)     # [(m, g, lo, hi)] all micro-batches
+    mine: list = field(default_factory=list)      # per minibatch: this rank's [(g, lo, hi)]
+
+    @property
+    def n_micro(self) -> int:
+        return len(self.micro)
+
+
+def lpt_assign(sizes, world_size: int):
+    """Longest-processing-time-first: deal items (by descending size, ties by index)
+    to the least-loaded rank (ties by rank).  Deterministic on every rank."""
+    order = sorted(range(len(sizes)), key=lambda i: (-int(sizes[i]), i))
+    heap = [(0, r) for r in range(world_size)]
+    owner = [0] * len(sizes)
+    for i in order:
+        load, r = heapq.heappop(heap)
+        owner[i] = r
+        heapq.heappush(heap, (load + int(sizes[i]), r))
+    return owner
+
+
+def shard_micro_batches(group_cu, n_groups, mb_offsets, world_size: int, rank: int):
+    """Host-side DP sharding of a replicated plan.
+
+    group_cu / n_groups / mb_offsets use the layout of areal_plan_microbatches.
+    Returns (all micro-batches [(m, g, lo, hi)], this rank's [(g, lo, hi)] per
+    minibatch), micro-batches dealt LPT by token count within each minibatch.
+    """
+    micro, mine = [], []
+    for m in range(len(n_groups)):
+        base = int(mb_offsets[m]) + m
+        groups = [(g, int(group_cu[base + g]), int(group_cu[base + g + 1]))
+                  for g in range(int(n_groups[m]))]
+        micro.extend((m, g, lo, hi) for g, lo, hi in groups)
+        owner = lpt_assign([hi - lo for _, lo, hi in groups], world_size)
+        mine.append([grp for grp, r in zip(groups, owner) if r == rank])
+    return micro, mine
+
+
+@dataclass
+class StepResult:
+    """TrainStepStats (trainer.py:273-282) fields + the raw per-minibatch sums."""
+    loss: float
+    clip_fraction: float
+    mean_ratio: float
+    tokens: int
+    minibatch_updates: int
+    microbatches: int
+    excluded_tokens: int
+    masked_tokens: int
+    entropy: float
+    minibatch_stats: np.ndarray   # [M, 8] all-reduced sums
+
+
+class DecoupledPPOStep:
+    """The hot path of one PPO step over a packed global batch (see module doc)."""
+
+    def __init__(self, config: HotPathConfig = HotPathConfig(), device=None, group=None):
+        self.cfg = config
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None \
+            else torch.device(device)
+        self.group = group
+        if dist.is_available() and dist.is_initialized():
+            self.world = dist.get_world_size(group)
+            self.rank = dist.get_rank(group)
+        else:
+            self.world, self.rank = 1, 0
+        self.launches = 0  # kernels launched by this object (K1-K5)
+        self.k1_events: list = []
+        self.k2_events: list = []
+        self.k2_bytes = 0
+        self.k1_bytes = 0
+        self.record_events = False
+
+    # ---- K3
+    def advantages(self, ro: PackedRollouts) -> torch.Tensor:
+        c = self.cfg
+        norm = ADV_NORM_ALIASES.get(c.adv_norm, c.adv_norm)
+        adv = K.advantages(ro.rewards, ro.traj_bounds, ro.n_tokens, mode=c.adv_mode,
+                           gamma=c.gamma, lam=c.lam, values=ro.values, norm=norm,
+                           group_ids=ro.group_ids, eps=c.adv_eps)
+        self.launches += 1 + (5 if norm == "global" else (1 if norm.startswith("group") else 0))
+        return adv
+
+    # ---- K4 + K5
+    def plan(self, ro: PackedRollouts) -> StepPlan:
+        c = self.cfg
+        items = minibatch_items(ro.traj_bounds_host, c.minibatches)
+        if not items:
+            return StepPlan(items, None, None, None, None)
+        lens = np.diff(ro.traj_bounds_host)
+        mb_offsets = np.concatenate([[0], np.cumsum([len(x) for x in items])]).astype(np.int32)
+        mb_tokens = [int(lens[x].sum()) for x in items]
+        mb_token_start = np.concatenate([[0], np.cumsum(mb_tokens)[:-1]]).astype(np.int64)
+        flat = torch.from_numpy(np.concatenate(items).astype(np.int32)).to(self.device)
+        dplan = K.plan_microbatches(ro.traj_bounds, flat, mb_offsets, mb_token_start,
+                                    c.micro_token_budget, c.micro_min_groups)
+        gather, _ = K.fill_gather(ro.traj_bounds, dplan, int(sum(mb_tokens)))
+        self.launches += 2
+        # the single host sync of the plan: micro-batch sizes drive the model's shapes
+        small = torch.cat([dplan.status[:len(items)].to(torch.int64),
+                           dplan.n_groups[:len(items)].to(torch.int64), dplan.group_cu]).cpu().numpy()
+        M = len(items)
+        status, n_groups, group_cu = small[:M], small[M:2 * M], small[2 * M:]
+        bad = np.nonzero(status)[0]
+        if len(bad):
+            m = int(bad[0])
+            raise _status_error(int(status[m]), [int(lens[k]) for k in items[m]],
+                                c.micro_token_budget)
+        sp = StepPlan(items, dplan, gather, group_cu, n_groups)
+        sp.micro, sp.mine = shard_micro_batches(group_cu, n_groups, mb_offsets, self.world,
+                                                self.rank)
+        return sp
+
+    def _timed(self, events, fn):
+        if not self.record_events:
+            return fn()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        out = fn()
+        e.record()
+        events.append((s, e))
+        return out
+
+    # ---- K1 over this rank's micro-batches (prox, once per global batch)
+    def prox_logprobs(self, ro: PackedRollouts, sp: StepPlan, logits_fn) -> torch.Tensor:
+        prox = torch.empty(ro.n_tokens, dtype=torch.float64, device=self.device)
+        for m, groups in enumerate(sp.mine):
+            for g, lo, hi in groups:
+                rows = sp.gather[lo:hi]
+                logits = logits_fn("prox", m, g, rows)
+                self._timed(self.k1_events, lambda: K.logprob_fwd(
+                    logits, ro.tokens, row_index=rows, lp_out=prox, with_entropy=False,
+                    algo=self.cfg.algo))
+                self.k1_bytes += (hi - lo) * (logits.shape[1] * logits.element_size() + 16)
+                self.launches += 1
+        return prox
+
+    # ---- full step
+    def run(self, ro: PackedRollouts, logits_fn, backward_fn=None, update_fn=None,
+            current_version: int = 0, dlogits_fn=None) -> StepResult:
+        c = self.cfg
+        adv = self.advantages(ro)                               # trainer.py:296
+        sp = self.plan(ro)                                      # 300-315
+        prox = self.prox_logprobs(ro, sp, logits_fn)            # 295 (before any update)
+        decoupled = c.objective == "decoupled"
+        M = len(sp.items)
+        mstats = torch.zeros((max(M, 1), K._lib.N_STATS), dtype=torch.float64, device=self.device)
+        micro_count = 0
+        for m in range(M):
+            st = mstats[m]
+            for g, lo, hi in sp.mine[m]:
+                rows = sp.gather[lo:hi]
+                logits = logits_fn("train", m, g, rows)
+                dl_buf = dlogits_fn(m, g, logits) if dlogits_fn else None
+                dl, _ = self._timed(self.k2_events, lambda: K.ppo_fwd_bwd(
+                    logits, ro.tokens, ro.behav, prox, adv, clip_eps=c.clip_eps,
+                    decoupled=decoupled, versions=ro.versions, current_version=current_version,
+                    eta_mask=c.eta_mask, behav_weight_cap=c.behav_weight_cap, row_index=rows,
+                    dlogits=dl_buf, stats=st, algo=c.algo))
+                self.k2_bytes += (hi - lo) * (2 * logits.shape[1] * logits.element_size() + 52)
+                self.launches += 1
+                if backward_fn is not None:
+                    backward_fn(m, g, dl)
+            micro_count += int(sp.n_groups[m])
+            if self.world > 1:
+                dist.all_reduce(st, group=self.group)           # the one collective
+            if update_fn is not None:
+                update_fn(m, st)                                # 329-331
+        s = mstats[:M].cpu().numpy() if M else np.zeros((0, 8))
+        tot = s.sum(axis=0) if M else np.zeros(8)
+        d = max(int(tot[1]), 1)
+        return StepResult(loss=-float(tot[0]) / d, clip_fraction=float(tot[2]) / d,
+                          mean_ratio=float(tot[3]) / d, tokens=ro.n_tokens,
+                          minibatch_updates=M, microbatches=micro_count,
+                          excluded_tokens=int(tot[4]), masked_tokens=int(tot[5]),
+                          entropy=float(tot[6]) / d, minibatch_stats=s)

@@ -1,0 +1,257 @@
+"""Torch-tensor front end of the C-ABI kernels (K1-K5).
+
+Every function takes CUDA tensors, validates dtype / device / contiguity,
+passes raw pointers plus ``torch.cuda.current_stream()`` to libareal_b200.so
+and returns CUDA tensors.  Launches are asynchronous; nothing here
+synchronises except ``MicrobatchPlan``-style host reads done by callers.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import AdvParams, PpoParams, check
+
+STAT_NAMES = ("objective_sum", "n_valid", "n_clipped", "ratio_sum", "n_excluded", "n_masked",
+              "entropy_sum", "n_tokens")
+ADV_MODES = {"reference": 0, "gae": 1}
+NORMS = {"none": 0, "global": 1, "group": 2, "group_token": 2, "group_sequence": 3}
+
+_WORKSPACES: dict = {}
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def workspace(device=None) -> torch.Tensor:
+    """Zero-initialised per-(device, stream) workspace (AREAL_WORKSPACE_BYTES)."""
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    key = (dev.index, torch.cuda.current_stream(dev).cuda_stream)
+    ws = _WORKSPACES.get(key)
+    if ws is None:
+        ws = torch.zeros(_lib.WORKSPACE_BYTES, dtype=torch.uint8, device=dev)
+        _WORKSPACES[key] = ws
+    return ws
+
+
+def _need(t, name, dtype, device=None, numel=None):
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor")
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if device is not None and t.device != device:
+        raise ValueError(f"{name} is on {t.device}, expected {device}")
+    if numel is not None and t.numel() < numel:
+        raise ValueError(f"{name} has {t.numel()} elements, needs >= {numel}")
+    return t
+
+
+def _logits_info(logits):
+    if not isinstance(logits, torch.Tensor) or not logits.is_cuda or logits.dim() != 2:
+        raise ValueError("logits must be a 2-D CUDA tensor [rows, vocab]")
+    if logits.dtype not in _lib.DTYPE_CODES:
+        raise TypeError(f"unsupported logits dtype {logits.dtype}")
+    if logits.stride(1) != 1:
+        raise ValueError("logits rows must be contiguous (stride(1) == 1)")
+    n, v = logits.shape
+    ld = logits.stride(0) if n > 1 else v
+    return n, v, ld, _lib.DTYPE_CODES[logits.dtype]
+
+
+# ---------------------------------------------------------------- K1
+def logprob_fwd(logits: torch.Tensor, tokens: torch.Tensor, row_index: torch.Tensor | None = None,
+                lp_out: torch.Tensor | None = None, entropy_out: torch.Tensor | None = None,
+                with_entropy: bool = True, algo: str = "auto"):
+    """Per-token log-prob (and entropy) of ``tokens`` under ``logits`` (K1).
+
+    Row r of ``logits`` belongs to global token ``row_index[r]`` (identity if
+    None); ``tokens``/``lp_out``/``entropy_out`` are indexed by global token.
+    Replaces trainer.recompute_prox_logprobs -> policy.batch_token_log_probs.
+    """
+    lib = _lib.load()
+    n, v, ld, dt = _logits_info(logits)
+    dev = logits.device
+    n_glob = tokens.numel()
+    _need(tokens, "tokens", torch.int64, dev)
+    if row_index is not None:
+        _need(row_index, "row_index", torch.int32, dev, n)
+    elif n_glob < n:
+        raise ValueError("tokens shorter than the number of logits rows")
+    if lp_out is None:
+        lp_out = torch.empty(n_glob, dtype=torch.float64, device=dev)
+    _need(lp_out, "lp_out", torch.float64, dev, n_glob)
+    if with_entropy and entropy_out is None:
+        entropy_out = torch.empty(n_glob, dtype=torch.float64, device=dev)
+    if entropy_out is not None:
+        _need(entropy_out, "entropy_out", torch.float64, dev, n_glob)
+    ws = workspace(dev)
+    check(lib.areal_logprob_fwd(_ptr(logits), ld, dt, n, v, _ptr(tokens), _ptr(row_index),
+                                _ptr(lp_out), _ptr(entropy_out), _lib.ALGO_CODES[algo],
+                                _ptr(ws), ws.numel(), _stream()), "areal_logprob_fwd")
+    return lp_out, entropy_out
+
+
+# ---------------------------------------------------------------- K2
+def ppo_fwd_bwd(logits, tokens, behav, prox, adv, *, clip_eps=0.2, decoupled=True,
+                versions=None, current_version=0, eta_mask=-1, behav_weight_cap=0.0,
+                grad_scale=1.0, row_index=None, dlogits=None, lp_out=None, entropy_out=None,
+                stats=None, algo="auto"):
+    """Fused decoupled/naive PPO loss + backward (K2).
+
+    Returns ``(dlogits, stats)``: dlogits = grad_scale * coef * (softmax - onehot)
+    (the gradient of -sum(objective) scaled), stats a float64[8] device tensor
+    accumulated with += (order: ``STAT_NAMES``).  ``dlogits`` may be ``logits``
+    itself (in-place backward).  Per-token arrays are float64 indexed by global
+    token (see ``row_index``).  Replaces trainer._surrogate_terms.
+    """
+    lib = _lib.load()
+    n, v, ld, dt = _logits_info(logits)
+    dev = logits.device
+    n_glob = tokens.numel()
+    _need(tokens, "tokens", torch.int64, dev)
+    _need(behav, "behav", torch.float64, dev, n_glob)
+    _need(adv, "adv", torch.float64, dev, n_glob)
+    if decoupled:
+        _need(prox, "prox", torch.float64, dev, n_glob)
+    if versions is not None:
+        _need(versions, "versions", torch.int32, dev, n_glob)
+    if row_index is not None:
+        _need(row_index, "row_index", torch.int32, dev, n)
+    elif n_glob < n:
+        raise ValueError("tokens shorter than the number of logits rows")
+    if dlogits is None:
+        dlogits = torch.empty_like(logits)
+    if dlogits.dtype != logits.dtype or dlogits.shape != logits.shape or dlogits.stride(1) != 1:
+        raise ValueError("dlogits must match logits in dtype/shape with unit column stride")
+    ld_out = dlogits.stride(0) if n > 1 else v
+    if stats is None:
+        stats = torch.zeros(_lib.N_STATS, dtype=torch.float64, device=dev)
+    _need(stats, "stats", torch.float64, dev, _lib.N_STATS)
+    for name, t in (("lp_out", lp_out), ("entropy_out", entropy_out)):
+        if t is not None:
+            _need(t, name, torch.float64, dev, n_glob)
+    p = PpoParams(float(clip_eps), float(behav_weight_cap), float(grad_scale), int(bool(decoupled)),
+                  int(eta_mask), int(current_version), _lib.ALGO_CODES[algo])
+    ws = workspace(dev)
+    check(lib.areal_ppo_fwd_bwd(_ptr(logits), ld, _ptr(dlogits), ld_out, dt, n, v, _ptr(tokens),
+                                _ptr(behav), _ptr(prox if decoupled else None), _ptr(adv),
+                                _ptr(versions), _ptr(row_index), ctypes.byref(p), _ptr(lp_out),
+                                _ptr(entropy_out), _ptr(stats), _ptr(ws), ws.numel(), _stream()),
+          "areal_ppo_fwd_bwd")
+    return dlogits, stats
+
+
+# ---------------------------------------------------------------- K3
+def advantages(rewards, traj_bounds, n_tokens: int, *, mode="reference", gamma=1.0, lam=1.0,
+               values=None, norm="global", group_ids=None, n_groups=None, eps=0.0, out=None,
+               returns_out=None, norm_stats=None):
+    """Per-token advantages (K3).  ``mode='reference'`` + ``norm='global'`` is
+    bit-identical to trainer.compute_advantages."""
+    lib = _lib.load()
+    dev = rewards.device
+    n_traj = rewards.numel()
+    _need(rewards, "rewards", torch.float64, dev)
+    _need(traj_bounds, "traj_bounds", torch.int64, dev, n_traj + 1)
+    if values is not None:
+        _need(values, "values", torch.float64, dev, n_tokens)
+    g = None
+    if norm in ("group", "group_token", "group_sequence"):
+        if group_ids is None:
+            raise ValueError("group normalisation needs group_ids")
+        g = _need(group_ids, "group_ids", torch.int32, dev, n_traj)
+        if n_groups is None:
+            n_groups = int(group_ids.max().item()) + 1 if n_traj else 0
+    if out is None:
+        out = torch.empty(n_tokens, dtype=torch.float64, device=dev)
+    _need(out, "out", torch.float64, dev, n_tokens)
+    p = AdvParams(float(gamma), float(lam), float(eps), ADV_MODES[mode], NORMS[norm])
+    ws = workspace(dev)
+    check(lib.areal_advantages(_ptr(rewards), _ptr(traj_bounds), n_traj, int(n_tokens),
+                               _ptr(values), _ptr(g), int(n_groups or 0), ctypes.byref(p),
+                               _ptr(out), _ptr(returns_out), _ptr(norm_stats), _ptr(ws),
+                               ws.numel(), _stream()), "areal_advantages")
+    return out
+
+
+# ---------------------------------------------------------------- K4 + K5
+@dataclass
+class DevicePlan:
+    """Device outputs of areal_plan_microbatches (+ the host inputs that sized them)."""
+    group_of: torch.Tensor
+    slot_of: torch.Tensor
+    n_groups: torch.Tensor
+    group_cu: torch.Tensor
+    group_seq_cu: torch.Tensor
+    packed_traj: torch.Tensor
+    seq_cu: torch.Tensor
+    status: torch.Tensor
+    mb_offsets: np.ndarray
+    mb_token_start: np.ndarray
+    n_packed_tokens: int
+
+
+def plan_microbatches(traj_bounds: torch.Tensor, item_traj: torch.Tensor, mb_offsets,
+                      mb_token_start, capacity: int, min_groups: int) -> DevicePlan:
+    """Dynamic micro-batch allocation for every minibatch at once (K4 + packing plan).
+
+    ``item_traj`` (device int32) lists the non-empty trajectories of each
+    minibatch back to back; ``mb_offsets`` (host, M+1) delimits them;
+    ``mb_token_start`` (host, M) is each minibatch's offset in the packed stream.
+    """
+    lib = _lib.load()
+    dev = traj_bounds.device
+    _need(traj_bounds, "traj_bounds", torch.int64, dev)
+    _need(item_traj, "item_traj", torch.int32, dev)
+    mb_offsets = np.asarray(mb_offsets, dtype=np.int32)
+    mb_token_start = np.asarray(mb_token_start, dtype=np.int64)
+    M = len(mb_offsets) - 1
+    n_items = int(mb_offsets[-1]) if M > 0 else 0
+    max_items = int(np.max(np.diff(mb_offsets))) if M > 0 else 0
+    if max_items > _lib.MAX_ITEMS_PER_MINIBATCH:
+        raise ValueError(f"{max_items} sequences in one minibatch exceeds "
+                         f"{_lib.MAX_ITEMS_PER_MINIBATCH}")
+    i32 = dict(dtype=torch.int32, device=dev)
+    mb_off_d = torch.from_numpy(mb_offsets).to(dev, non_blocking=True)
+    mb_tok_d = torch.from_numpy(mb_token_start).to(dev, non_blocking=True)
+    plan = DevicePlan(
+        group_of=torch.empty(n_items, **i32), slot_of=torch.empty(n_items, **i32),
+        n_groups=torch.empty(max(M, 1), **i32),
+        group_cu=torch.empty(n_items + M, dtype=torch.int64, device=dev),
+        group_seq_cu=torch.empty(n_items + M, **i32), packed_traj=torch.empty(n_items, **i32),
+        seq_cu=torch.empty(n_items + 1, dtype=torch.int64, device=dev),
+        status=torch.zeros(max(M, 1), **i32), mb_offsets=mb_offsets,
+        mb_token_start=mb_token_start, n_packed_tokens=0)
+    check(lib.areal_plan_microbatches(
+        _ptr(traj_bounds), _ptr(item_traj), _ptr(mb_off_d), _ptr(mb_tok_d), M, n_items, max_items,
+        int(capacity), int(min_groups), _ptr(plan.group_of), _ptr(plan.slot_of),
+        _ptr(plan.n_groups), _ptr(plan.group_cu), _ptr(plan.group_seq_cu),
+        _ptr(plan.packed_traj), _ptr(plan.seq_cu), _ptr(plan.status), _stream()),
+        "areal_plan_microbatches")
+    plan._keepalive = (mb_off_d, mb_tok_d)  # host->device copies are async
+    return plan
+
+
+def fill_gather(traj_bounds, plan: DevicePlan, n_packed_tokens: int, with_seq_id=False):
+    """Packed gather index (K5): gather[p] = global token index at packed position p."""
+    lib = _lib.load()
+    dev = traj_bounds.device
+    gather = torch.empty(n_packed_tokens, dtype=torch.int32, device=dev)
+    seq_id = torch.empty(n_packed_tokens, dtype=torch.int32, device=dev) if with_seq_id else None
+    n_items = plan.packed_traj.numel()
+    check(lib.areal_fill_gather(_ptr(traj_bounds), _ptr(plan.packed_traj), _ptr(plan.seq_cu),
+                                n_items, int(n_packed_tokens), _ptr(gather), _ptr(seq_id),
+                                _stream()), "areal_fill_gather")
+    return gather, seq_id
