@@ -231,11 +231,16 @@ def run_ours(args, cfg):
         bufs.append(b)
     dl_buf = torch.empty((C, V), dtype=ldt, device=dev)
     counter = [0]
+    micro_id = {}
 
     def logits_fn(phase, m, g, rows):
-        b = bufs[counter[0] % n_buf]
+        # the same micro-batch sees the same synthetic logits in the prox and train
+        # phases (a model whose weights did not move); micro-batches rotate buffers
+        key = (m, g)
+        if key not in micro_id:
+            micro_id[key] = len(micro_id)
         counter[0] += 1
-        return b[: rows.numel()]
+        return bufs[micro_id[key] % n_buf][: rows.numel()]
 
     def dlogits_fn(m, g, logits):
         return dl_buf[: logits.shape[0]]

@@ -287,7 +287,7 @@ __device__ __forceinline__ void row_warp_body(const PpoArgs& a) {
       if (BWD) {
         const TokenTerms t = ppo_token(lp, a.behav[idx], a.prox ? a.prox[idx] : 0.0, a.adv[idx],
                                        a.versions ? a.versions[idx] : 0, a);
-        stats_add(st, t, ent);
+        stats_add(st, t, a.ent_out ? ent : 0.0);
         gc = a.grad_scale * t.coef;
       }
     }
@@ -324,25 +324,125 @@ __device__ __forceinline__ void row_warp_body(const PpoArgs& a) {
 
 // ================================================================== row_ring kernel
 constexpr int kChunkBytes = 16384;
-constexpr int kConsumerWarps = 8;
+constexpr int kConsumerWarps = 16;
 constexpr int kConsumers = kConsumerWarps * 32;
 constexpr int kRingThreads = kConsumers + 32;  // + 1 producer warp
 constexpr int kBarConsumers = 1;                // named barrier id among consumer warps
+constexpr int kVecPerThread = kChunkBytes / 16 / kConsumers;  // 16-byte vectors per thread per chunk
+constexpr int kWarpBytes = kChunkBytes / kConsumerWarps;      // contiguous bytes a warp owns per chunk
 
 struct RingSmemTail {
-  uint64_t xbar[2];           // DSMEM exchange barriers (double-buffered by row parity)
-  double xval[2][8][3];       // [parity][rank][m, s, sx]
-  double red[kConsumerWarps][3];
-  double bc_gc;               // broadcast: grad_scale * coef
-  double bc_lse;              // broadcast: lse in shift units
+  uint64_t xbar[2];                 // DSMEM exchange barriers (double-buffered by row parity)
+  double xval[2][8][3];             // [parity][rank][m, s, sx]
+  float redf[2][kConsumerWarps][3]; // per-warp partials, double-buffered by row parity
+  double redd[2][kConsumerWarps][3];
+  double bc_gc;                     // broadcast: grad_scale * coef
+  double bc_lse;                    // broadcast: lse in shift units
+  long long bc_tok;                 // broadcast: token id
+  unsigned long long bc_dtok;       // broadcast: dlogit of the token element (T bits)
 };
 
-template <typename T, bool BWD>
+template <typename A> __device__ __forceinline__ A* red_ptr(RingSmemTail* t, int par);
+template <> __device__ __forceinline__ float* red_ptr<float>(RingSmemTail* t, int par) {
+  return &t->redf[par][0][0];
+}
+template <> __device__ __forceinline__ double* red_ptr<double>(RingSmemTail* t, int par) {
+  return &t->redd[par][0][0];
+}
+
+// Ring cursor: slot index and mbarrier phase parity, advanced without division.
+struct Cursor {
+  uint32_t slot, phase;
+  __device__ __forceinline__ void next(uint32_t nslots) {
+    if (++slot == nslots) {
+      slot = 0;
+      phase ^= 1u;
+    }
+  }
+};
+
+// Vector j (< kVecPerThread) of this thread inside a chunk: each warp owns a
+// contiguous kWarpBytes region, lanes read consecutive 16-byte vectors.
+__device__ __forceinline__ int vec_index(int warp, int lane, int j) {
+  return warp * (kWarpBytes / 16) + j * 32 + lane;
+}
+
+template <typename T, bool ENT>
+__device__ __forceinline__ void fold_values(RowStat<typename Traits<T>::Acc>& rs,
+                                            const typename Traits<T>::Acc* f) {
+  using A = typename Traits<T>::Acc;
+  constexpr int N = kVecPerThread * Vec<T>::N;
+  A lmax = f[0];
+#pragma unroll
+  for (int i = 1; i < N; ++i) lmax = fmax(lmax, f[i]);
+  const A mn = fmax(rs.m, lmax);
+  const A muse = (mn == Lim<A>::ninf()) ? A(0) : mn;
+  const A c = Ex<A>::shift(muse);
+  const A r = Ex<A>::e(rs.m, c);  // rescale of the running sums (0 while m = -inf)
+  A s0 = A(0), s1 = A(0), x0 = A(0), x1 = A(0);
+#pragma unroll
+  for (int i = 0; i < N; i += 2) {
+    const A e0 = Ex<A>::e(f[i], c), e1 = Ex<A>::e(f[i + 1], c);
+    s0 += e0;
+    s1 += e1;
+    if (ENT) {
+      x0 += e0 * fmax(f[i], Lim<A>::lowest());  // p log p := 0 at p = 0
+      x1 += e1 * fmax(f[i + 1], Lim<A>::lowest());
+    }
+  }
+  rs.s = rs.s * r + (s0 + s1);
+  if (ENT) rs.sx = rs.sx * r + (x0 + x1);
+  rs.m = mn;
+}
+
+// Load this thread's vectors of a chunk (n valid vectors) as accumulation values.
+template <typename T>
+__device__ __forceinline__ void load_values(const uint4* q, int warp, int lane, int nvec,
+                                            typename Traits<T>::Acc* f) {
+  using A = typename Traits<T>::Acc;
+  constexpr int E = Vec<T>::N;
+  if (nvec == kChunkBytes / 16) {
+#pragma unroll
+    for (int j = 0; j < kVecPerThread; ++j) {
+      A g[E];
+      Vec<T>::unpack(q[vec_index(warp, lane, j)], g);
+#pragma unroll
+      for (int e = 0; e < E; ++e) f[j * E + e] = g[e];
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < kVecPerThread; ++j) {
+      const int vi = vec_index(warp, lane, j);
+      A g[E];
+      if (vi < nvec) {
+        Vec<T>::unpack(q[vi], g);
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) g[e] = Lim<A>::ninf();
+      }
+#pragma unroll
+      for (int e = 0; e < E; ++e) f[j * E + e] = g[e];
+    }
+  }
+}
+
+template <typename T> __device__ __forceinline__ unsigned long long to_bits(T v) {
+  unsigned long long b = 0;
+  memcpy(&b, &v, sizeof(T));
+  return b;
+}
+template <typename T> __device__ __forceinline__ T from_bits(unsigned long long b) {
+  T v;
+  memcpy(&v, &b, sizeof(T));
+  return v;
+}
+
+template <typename T, bool BWD, bool ENT>
 __device__ __forceinline__ void row_ring_body(const PpoArgs& a) {
   using A = typename Traits<T>::Acc;
   constexpr int E = Vec<T>::N;                 // elements per 16 bytes
   extern __shared__ __align__(1024) unsigned char smem[];
-  const int nslots = a.nslots;
+  const uint32_t nslots = (uint32_t)a.nslots;
   unsigned char* ring = smem;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)nslots * kChunkBytes);
   uint64_t* empty = full + nslots;
@@ -360,9 +460,9 @@ __device__ __forceinline__ void row_ring_body(const PpoArgs& a) {
   const int64_t slice_e0 = b16 * E;  // first vocab element of this rank's slice
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < nslots; ++s) {
+    for (uint32_t s = 0; s < nslots; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], BWD ? 1 : kConsumerWarps);
+      mbar_init(&empty[s], kConsumerWarps);  // one arrive per consumer warp per use
     }
     mbar_init(&tail->xbar[0], CS);
     mbar_init(&tail->xbar[1], CS);
@@ -379,170 +479,191 @@ __device__ __forceinline__ void row_ring_body(const PpoArgs& a) {
   if (tid >= kConsumers) {
     // ---------------- producer warp: one elected lane issues the TMA bulk loads
     if (tid == kConsumers) {
-      uint32_t k = 0;
+      Cursor cur = {0u, 0u};
+      uint32_t used = 0;  // slots filled at least once (no wait needed on first use)
       for (int64_t row = cid; row < a.n_rows; row += ncl) {
         const char* src = a.logits + row * a.ld_in_bytes + b16 * 16;
-        for (int c = 0; c < nchunks; ++c, ++k) {
-          const uint32_t slot = k % nslots, round = k / nslots;
-          if (round > 0) mbar_wait(&empty[slot], (round - 1) & 1);
+        for (int c = 0; c < nchunks; ++c) {
+          if (used >= nslots) mbar_wait(&empty[cur.slot], cur.phase ^ 1u);
+          else ++used;
           const uint32_t bytes = (uint32_t)min((int64_t)kChunkBytes, slice_bytes - (int64_t)c * kChunkBytes);
-          mbar_arrive_expect_tx(&full[slot], bytes);
-          bulk_g2s(ring + (size_t)slot * kChunkBytes, src + (size_t)c * kChunkBytes, bytes, &full[slot]);
+          mbar_arrive_expect_tx(&full[cur.slot], bytes);
+          bulk_g2s(ring + (size_t)cur.slot * kChunkBytes, src + (size_t)c * kChunkBytes, bytes,
+                   &full[cur.slot]);
+          cur.next(nslots);
         }
       }
     }
   } else {
     // ---------------- consumer warps
     const int warp = tid >> 5, lane = tid & 31;
-    uint32_t k = 0;        // ring position of this row's first chunk
-    uint32_t pending = 0;  // BWD: stores issued whose slot is not yet released (thread 0)
-    uint32_t pend_k = 0;
+    Cursor cur = {0u, 0u};     // first chunk of the current row
+    bool pending = false;      // BWD, lane 0: last store's slot not yet released
+    uint32_t pend_slot = 0;
     int it = 0;
     for (int64_t row = cid; row < a.n_rows; row += ncl, ++it) {
+      const int par = it & 1;
       const T* xrow = reinterpret_cast<const T*>(a.logits + row * a.ld_in_bytes);
       const int64_t idx = a.row_index ? (int64_t)a.row_index[row] : row;
       int64_t tok = 0;
-      double xa = 0.0;
-      if (tid == 0) {
+      double xa = 0.0, t_behav = 0.0, t_prox = 0.0, t_adv = 0.0;
+      int t_ver = 0;
+      if (tid == 0) {  // issue the per-token loads now; their latency hides behind pass 1
         tok = a.tokens[idx];
         xa = token_logit<T>(a, xrow, tok);
+        if (BWD) {
+          t_behav = a.behav[idx];
+          t_prox = a.prox ? a.prox[idx] : 0.0;
+          t_adv = a.adv[idx];
+          t_ver = a.versions ? a.versions[idx] : 0;
+        }
       }
-      // ---- pass 1: online (max, sum, sum*x) over the resident chunks
+      // ---- pass 1: online (max, sum e, sum e*x) over the chunks as they land
       RowStat<A> rs;
       rs.init();
+      Cursor cc = cur;
       for (int c = 0; c < nchunks; ++c) {
-        const uint32_t kk = k + c, slot = kk % nslots, round = kk / nslots;
-        mbar_wait(&full[slot], round & 1);
+        mbar_wait(&full[cc.slot], cc.phase);
         const int nvec = (int)(min((int64_t)kChunkBytes, slice_bytes - (int64_t)c * kChunkBytes) / 16);
-        const uint4* q = reinterpret_cast<const uint4*>(ring + (size_t)slot * kChunkBytes);
-        constexpr int kPer = kChunkBytes / 16 / kConsumers;  // vectors per thread per full chunk
-        A v[kPer * E];
-        A lmax = Lim<A>::ninf();
-#pragma unroll
-        for (int j = 0; j < kPer; ++j) {
-          const int vi = tid + j * kConsumers;
-          A f[E];
-          if (vi < nvec) {
-            Vec<T>::unpack(q[vi], f);
-          } else {
-#pragma unroll
-            for (int e = 0; e < E; ++e) f[e] = Lim<A>::ninf();
-          }
-#pragma unroll
-          for (int e = 0; e < E; ++e) {
-            v[j * E + e] = f[e];
-            lmax = fmax(lmax, f[e]);
-          }
-        }
-        fold(rs, v, lmax);
-        if (!BWD) {
+        const uint4* q = reinterpret_cast<const uint4*>(ring + (size_t)cc.slot * kChunkBytes);
+        A f[kVecPerThread * E];
+        load_values<T>(q, warp, lane, nvec, f);
+        if (!BWD) {  // K1: the slot is free as soon as the values are in registers
           __syncwarp();
-          if (lane == 0) mbar_arrive(&empty[slot]);
+          if (lane == 0) mbar_arrive(&empty[cc.slot]);
         }
+        fold_values<T, ENT>(rs, f);
+        cc.next(nslots);
       }
-      // ---- CTA reduce (fixed order)
+      // ---- CTA reduce: warp shuffles, then warp 0 merges the warp partials (fixed order)
       rs.warp_reduce();
+      A* red = red_ptr<A>(tail, par);
       if (lane == 0) {
-        tail->red[warp][0] = (double)rs.m;
-        tail->red[warp][1] = (double)rs.s;
-        tail->red[warp][2] = (double)rs.sx;
+        red[warp * 3 + 0] = rs.m;
+        red[warp * 3 + 1] = rs.s;
+        red[warp * 3 + 2] = rs.sx;
       }
       named_bar_sync(kBarConsumers, kConsumers);
-      if (tid == 0) {
-        RowStat<A> cta;
-        cta.init();
-        for (int w = 0; w < kConsumerWarps; ++w)
-          cta.merge((A)tail->red[w][0], (A)tail->red[w][1], (A)tail->red[w][2]);
-        RowStat<A> tot = cta;
-        if (CS > 1) {
-          // ---- cluster exchange through DSMEM: write my partial into every
-          // rank's slot [parity][my rank], release-arrive on its barrier.
-          const int par = it & 1;
-          for (int r = 0; r < CS; ++r) {
-            const uint32_t base = mapa_shared(smem_u32(&tail->xval[par][rank][0]), (uint32_t)r);
-            st_cluster_f64(base, (double)cta.m);
-            st_cluster_f64(base + 8, (double)cta.s);
-            st_cluster_f64(base + 16, (double)cta.sx);
-            mbar_remote_arrive_release(mapa_shared(smem_u32(&tail->xbar[par]), (uint32_t)r));
+      if (warp == 0) {
+        RowStat<A> w;
+        if (lane < kConsumerWarps) {
+          w.m = red[lane * 3 + 0];
+          w.s = red[lane * 3 + 1];
+          w.sx = red[lane * 3 + 2];
+        } else {
+          w.init();
+        }
+        w.warp_reduce();
+        if (lane == 0) {
+          RowStat<A> tot = w;
+          if (CS > 1) {
+            // ---- cluster exchange through DSMEM: write my partial into every
+            // rank's slot [parity][my rank], release-arrive on its barrier.
+            for (int r = 0; r < CS; ++r) {
+              const uint32_t base = mapa_shared(smem_u32(&tail->xval[par][rank][0]), (uint32_t)r);
+              st_cluster_f64(base, (double)w.m);
+              st_cluster_f64(base + 8, (double)w.s);
+              st_cluster_f64(base + 16, (double)w.sx);
+              mbar_remote_arrive_release(mapa_shared(smem_u32(&tail->xbar[par]), (uint32_t)r));
+            }
+            mbar_wait_cluster(&tail->xbar[par], (it >> 1) & 1);
+            tot.init();
+            for (int r = 0; r < CS; ++r)
+              tot.merge((A)tail->xval[par][r][0], (A)tail->xval[par][r][1], (A)tail->xval[par][r][2]);
           }
-          mbar_wait_cluster(&tail->xbar[par], (it >> 1) & 1);
-          tot.init();
-          for (int r = 0; r < CS; ++r)
-            tot.merge((A)tail->xval[par][r][0], (A)tail->xval[par][r][1], (A)tail->xval[par][r][2]);
+          const A lse_s = Ex<A>::lse_shift(tot.m == Lim<A>::ninf() ? A(0) : tot.m, tot.s);
+          const double lse = Ex<A>::lse_nat(lse_s);
+          const double ent = ENT ? lse - (double)(tot.sx / tot.s) : 0.0;
+          const double lp = xa - lse;
+          double gc = 0.0;
+          if (rank == 0) {
+            if (a.lp_out) a.lp_out[idx] = lp;
+            if (ENT && a.ent_out) a.ent_out[idx] = ent;
+          }
+          if (BWD) {
+            const TokenTerms t = ppo_token(lp, t_behav, t_prox, t_adv, t_ver, a);
+            if (rank == 0) stats_add(st, t, ent);
+            gc = a.grad_scale * t.coef;
+            tail->bc_gc = gc;
+            tail->bc_lse = (double)lse_s;
+            tail->bc_tok = tok;
+            // the token's own element: g * (p - 1), from the exact lp
+            tail->bc_dtok = to_bits<T>(Traits<T>::from_acc((A)(gc * (exp(lp) - 1.0))));
+          }
         }
-        const A lse_s = Ex<A>::lse_shift(tot.m == Lim<A>::ninf() ? A(0) : tot.m, tot.s);
-        const double lse = Ex<A>::lse_nat(lse_s);
-        const double ent = lse - (double)(tot.sx / tot.s);
-        const double lp = xa - lse;
-        double gc = 0.0;
-        if (rank == 0) {
-          if (a.lp_out) a.lp_out[idx] = lp;
-          if (a.ent_out) a.ent_out[idx] = ent;
-        }
-        if (BWD) {
-          const TokenTerms t = ppo_token(lp, a.behav[idx], a.prox ? a.prox[idx] : 0.0, a.adv[idx],
-                                         a.versions ? a.versions[idx] : 0, a);
-          if (rank == 0) stats_add(st, t, ent);
-          gc = a.grad_scale * t.coef;
-        }
-        tail->bc_gc = gc;
-        tail->bc_lse = (double)lse_s;
-        tail->red[0][0] = __longlong_as_double(tok);  // token id broadcast
       }
       if (BWD) {
         named_bar_sync(kBarConsumers, kConsumers);
         const A g = (A)tail->bc_gc;
         const A lse_s = (A)tail->bc_lse;
-        const int64_t tok_local = __double_as_longlong(tail->red[0][0]) - slice_e0;
+        const int64_t tok_local = tail->bc_tok - slice_e0;  // may lie outside this slice
+        const T dtok = from_bits<T>(tail->bc_dtok);
         char* drow = a.dlogits + row * a.ld_out_bytes + b16 * 16;
-        // ---- pass 2: dlogits in place, then bulk store
+        // ---- pass 2: dlogits = g * (softmax - onehot) in place; each warp stores
+        // its own contiguous part of the chunk and recycles the slot itself.
+        cc = cur;
         for (int c = 0; c < nchunks; ++c) {
-          const uint32_t kk = k + c, slot = kk % nslots;
           const int cbytes = (int)min((int64_t)kChunkBytes, slice_bytes - (int64_t)c * kChunkBytes);
           const int nvec = cbytes / 16;
-          uint4* q = reinterpret_cast<uint4*>(ring + (size_t)slot * kChunkBytes);
-          constexpr int kPer = kChunkBytes / 16 / kConsumers;
+          uint4* q = reinterpret_cast<uint4*>(ring + (size_t)cc.slot * kChunkBytes);
+          if (g == A(0)) {  // no gradient through this token: zeros, no exponentials
 #pragma unroll
-          for (int j = 0; j < kPer; ++j) {
-            const int vi = tid + j * kConsumers;
-            if (vi < nvec) {
-              A f[E];
-              Vec<T>::unpack(q[vi], f);
-              const int64_t e0 = (int64_t)c * (kChunkBytes / sizeof(T)) + (int64_t)vi * E;
+            for (int j = 0; j < kVecPerThread; ++j) {
+              const int vi = vec_index(warp, lane, j);
+              if (vi < nvec) q[vi] = make_uint4(0, 0, 0, 0);
+            }
+          } else {
 #pragma unroll
-              for (int e = 0; e < E; ++e) {
-                A p;
-                if constexpr (std::is_same<A, float>::value)
-                  p = fast_exp2(fmaf(f[e], Lim<float>::kLog2e, -lse_s));
-                else
-                  p = exp(f[e] - lse_s);
-                f[e] = g * (p - ((e0 + e) == tok_local ? A(1) : A(0)));
+            for (int j = 0; j < kVecPerThread; ++j) {
+              const int vi = vec_index(warp, lane, j);
+              if (nvec == kChunkBytes / 16 || vi < nvec) {
+                A f[E];
+                Vec<T>::unpack(q[vi], f);
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                  A p;
+                  if constexpr (std::is_same<A, float>::value)
+                    p = fast_exp2(fmaf(f[e], Lim<float>::kLog2e, -lse_s));
+                  else
+                    p = exp(f[e] - lse_s);
+                  f[e] = g * p;
+                }
+                q[vi] = Vec<T>::pack(f);
               }
-              q[vi] = Vec<T>::pack(f);
+            }
+            // the one-hot element: written by the thread that owns it
+            const int64_t toff = tok_local - (int64_t)c * (kChunkBytes / (int)sizeof(T));
+            if (toff >= 0 && toff < (int64_t)cbytes / (int64_t)sizeof(T)) {
+              const int tv = (int)(toff / E);
+              if (tv / (kWarpBytes / 16) == warp && (tv % 32) == lane)
+                reinterpret_cast<T*>(q)[toff] = dtok;
             }
           }
           fence_proxy_async_smem();
-          named_bar_sync(kBarConsumers, kConsumers);
-          if (tid == 0) {
-            bulk_s2g(drow + (size_t)c * kChunkBytes, ring + (size_t)slot * kChunkBytes, (uint32_t)cbytes);
-            bulk_commit();
-            if (pending) {
-              // the previous store must have finished reading its slot before reuse
-              bulk_wait_read<1>();
-              mbar_arrive(&empty[pend_k % nslots]);
+          __syncwarp();
+          if (lane == 0) {
+            const int wb0 = warp * kWarpBytes;
+            if (wb0 < cbytes) {
+              const int wbytes = min(kWarpBytes, cbytes - wb0);
+              bulk_s2g(drow + (size_t)c * kChunkBytes + wb0,
+                       ring + (size_t)cc.slot * kChunkBytes + wb0, (uint32_t)wbytes);
             }
-            pending = 1;
-            pend_k = kk;
+            bulk_commit();
+            if (pending) {  // previous store has read its slot -> release it
+              bulk_wait_read<1>();
+              mbar_arrive(&empty[pend_slot]);
+            }
+            pending = true;
+            pend_slot = cc.slot;
           }
+          cc.next(nslots);
         }
-      } else {
-        named_bar_sync(kBarConsumers, kConsumers);  // protect tail->red reuse across rows
       }
-      k += nchunks;
+      cur = cc;
     }
-    if (BWD && tid == 0) {
+    if (BWD && lane == 0) {
       bulk_wait<0>();  // all dlogits stores complete before the CTA retires
-      if (pending) mbar_arrive(&empty[pend_k % nslots]);
+      if (pending) mbar_arrive(&empty[pend_slot]);
     }
   }
   // all threads: final stats reduction (rank-0 CTAs carry the counters)
@@ -568,13 +689,13 @@ template <typename T>
 __global__ void __launch_bounds__(kWarpKernelWarps * 32) ppo_warp_kernel(PpoArgs a) {
   row_warp_body<T, true>(a);
 }
-template <typename T>
+template <typename T, bool ENT>
 __global__ void __launch_bounds__(kRingThreads, 1) logprob_ring_kernel(PpoArgs a) {
-  row_ring_body<T, false>(a);
+  row_ring_body<T, false, ENT>(a);
 }
-template <typename T>
+template <typename T, bool ENT>
 __global__ void __launch_bounds__(kRingThreads, 1) ppo_ring_kernel(PpoArgs a) {
-  row_ring_body<T, true>(a);
+  row_ring_body<T, true, ENT>(a);
 }
 
 // ================================================================== host side
@@ -604,7 +725,7 @@ static int max_slots(const DevInfo& d) {
   return n;
 }
 
-template <typename T, bool BWD>
+template <typename T, bool BWD, bool ENT>
 static int launch_ring(PpoArgs a, cudaStream_t stream, int cs_force) {
   DevInfo d = get_dev();
   const int nslots = max_slots(d);
@@ -629,7 +750,7 @@ static int launch_ring(PpoArgs a, cudaStream_t stream, int cs_force) {
   a.slice16 = (V16 + CS - 1) / CS;
   a.nslots = nslots;
   const size_t smem = ring_smem_bytes(nslots);
-  auto kern = BWD ? ppo_ring_kernel<T> : logprob_ring_kernel<T>;
+  auto kern = BWD ? ppo_ring_kernel<T, ENT> : logprob_ring_kernel<T, ENT>;
   static thread_local int attr_set[16] = {0};
   int dev = d.dev & 15;
   if (!(attr_set[dev] & 1)) {
@@ -703,11 +824,12 @@ static int dispatch(PpoArgs a, int dtype, int algo, cudaStream_t stream) {
   }
   if (ring) {
     int rc;
+    const bool ent = a.ent_out != nullptr;
     switch (dtype) {
-      case AREAL_F32: rc = launch_ring<float, BWD>(a, stream, 0); break;
-      case AREAL_BF16: rc = launch_ring<__nv_bfloat16, BWD>(a, stream, 0); break;
-      case AREAL_F16: rc = launch_ring<__half, BWD>(a, stream, 0); break;
-      case AREAL_F64: rc = launch_ring<double, BWD>(a, stream, 0); break;
+      case AREAL_F32: rc = ent ? launch_ring<float, BWD, true>(a, stream, 0) : launch_ring<float, BWD, false>(a, stream, 0); break;
+      case AREAL_BF16: rc = ent ? launch_ring<__nv_bfloat16, BWD, true>(a, stream, 0) : launch_ring<__nv_bfloat16, BWD, false>(a, stream, 0); break;
+      case AREAL_F16: rc = ent ? launch_ring<__half, BWD, true>(a, stream, 0) : launch_ring<__half, BWD, false>(a, stream, 0); break;
+      case AREAL_F64: rc = ent ? launch_ring<double, BWD, true>(a, stream, 0) : launch_ring<double, BWD, false>(a, stream, 0); break;
       default: return AREAL_ERR_BAD_DTYPE;
     }
     if (rc != AREAL_ERR_UNSUPPORTED || algo == AREAL_ALGO_ROW_RING) return rc;

@@ -1,0 +1,82 @@
+"""LM-scale hot path (hotpath.DecoupledPPOStep.run, the call bench.py measures)
+vs the oracle's train_step structure (trainer.py:285-346) on given logits."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_2505_24298_b200.hotpath import DecoupledPPOStep, HotPathConfig, PackedRollouts
+
+
+def _setup(n=40, V=2048, lo=5, hi=300, seed=0, dtype=torch.bfloat16):
+    rng = np.random.default_rng(seed)
+    lengths = rng.integers(lo, hi, size=n)
+    lengths[3] = 0  # empty trajectory is skipped (trainer.py:310)
+    bounds = np.concatenate([[0], np.cumsum(lengths)]).astype(np.int64)
+    T = int(bounds[-1])
+    g = torch.Generator().manual_seed(seed)
+    # one logits row per global token, fixed across phases ("model" output)
+    table = (torch.randn(T, V, generator=g, dtype=torch.float64) * 2).to(dtype)
+    x64 = table.double().numpy()
+    tokens = rng.integers(0, V, size=T)
+    lp = O.token_logprobs(x64, tokens)
+    behav = lp + rng.normal(0, 0.3, size=T)
+    rewards = rng.choice([5.0, -5.0], size=n)
+    versions = rng.integers(5, 10, size=T).astype(np.int32)
+    return bounds, T, V, table, x64, tokens, behav, rewards, versions
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_run_matches_oracle_minibatch_sums(dtype):
+    bounds, T, V, table, x64, tokens, behav, rewards, versions = _setup(dtype=dtype)
+    cfg = HotPathConfig(minibatches=3, micro_token_budget=700, micro_min_groups=2,
+                        eta_mask=3)
+    ro = PackedRollouts.from_host(bounds, tokens, behav, rewards, versions=versions)
+    dev_table = table.cuda()
+    seen = []
+
+    def logits_fn(phase, m, g, rows):
+        seen.append((phase, m, g, rows.numel()))
+        return dev_table.index_select(0, rows.long())
+
+    grads = {}
+
+    def backward_fn(m, g, dl):
+        grads[(m, g)] = dl.double().cpu().numpy()
+
+    runner = DecoupledPPOStep(cfg)
+    res = runner.run(ro, logits_fn, backward_fn=backward_fn, current_version=10)
+    plan = O.train_step_plan(bounds, 3, 700, 2)
+    adv = O.compute_advantages_ref(rewards, bounds)
+    prox = O.token_logprobs(x64, tokens)
+    tol = 1e-5 if dtype == torch.float32 else 2e-2
+    assert res.minibatch_updates == len(plan)
+    assert res.microbatches == sum(len(mb["groups"]) for mb in plan)
+    for m, mb in enumerate(plan):
+        idx = np.concatenate(mb["gather"])
+        ref = O.surrogate_terms(x64[idx], tokens[idx], behav[idx], prox[idx], adv[idx],
+                                versions=versions[idx], current_version=10, eta_mask=3)
+        got = res.minibatch_stats[m]
+        assert got[1] == ref["stats"][1] and got[5] == ref["stats"][5] and got[7] == len(idx)
+        assert abs(got[0] - ref["stats"][0]) <= tol * max(1.0, abs(ref["stats"][0]))
+        for g, gi in enumerate(mb["gather"]):
+            r = O.surrogate_terms(x64[gi], tokens[gi], behav[gi], prox[gi], adv[gi],
+                                  versions=versions[gi], current_version=10, eta_mask=3)
+            d = grads[(m, g)]
+            assert np.allclose(d, r["dlogits"], rtol=tol, atol=tol * 1e-2)
+    # prox pass covers every micro-batch before any train-phase forward
+    phases = [p for p, *_ in seen]
+    assert phases.index("train") == phases.count("prox")
+
+
+def test_run_rejects_oversized_sequences():
+    from paper_2505_24298_b200.trainer import BatchError
+    bounds, T, V, table, x64, tokens, behav, rewards, versions = _setup(n=6, V=64, lo=50, hi=90)
+    ro = PackedRollouts.from_host(bounds, tokens, behav, rewards)
+    with pytest.raises(BatchError, match="exceeds capacity"):
+        DecoupledPPOStep(HotPathConfig(micro_token_budget=40)).run(
+            ro, lambda *a: None)

@@ -115,6 +115,24 @@ def test_ppo_fwd_bwd_matches_oracle(dt, V, algo, decoupled):
     check_k2(dt, dl, st, ref, T)
 
 
+@pytest.mark.parametrize("dt", ["f32", "bf16"])
+@pytest.mark.parametrize("algo", ["warp", "ring"])
+def test_ppo_entropy_outputs_and_stat(dt, algo):
+    T, V = 70, 151936 if algo == "ring" else 5000
+    logits, x64, tokens, behav, prox, adv = make_case(T, V, dt, seed=21)
+    ent = torch.empty(T, dtype=torch.float64, device="cuda")
+    dl, st = K.ppo_fwd_bwd(logits.cuda(), cuda(tokens), cuda(behav), cuda(prox), cuda(adv),
+                           entropy_out=ent, algo=algo)
+    ref = O.surrogate_terms(x64, tokens, behav, prox, adv)
+    assert np.allclose(ent.cpu().numpy(), ref["entropy"], rtol=1e-5, atol=1e-4)
+    assert st[6].item() == pytest.approx(ref["stats"][6], rel=1e-5)
+    check_k2(dt, dl.to(torch.float64).cpu().numpy(), st.cpu().numpy(), ref, T)
+    _, st2 = K.ppo_fwd_bwd(logits.cuda(), cuda(tokens), cuda(behav), cuda(prox), cuda(adv),
+                           algo=algo)
+    assert st2[6].item() == 0.0  # entropy is computed only when requested
+    assert torch.equal(st2[:6], st[:6])
+
+
 @pytest.mark.parametrize("algo", ["warp", "ring"])
 def test_ppo_masks_and_scale(algo):
     T, V = 80, 8192
