@@ -205,10 +205,16 @@ def run_ours(args, cfg):
         cpu_base = cpu_baseline(cfg["vocab"], target_s=args.cpu_seconds)  # before CUDA init
         cpu_base.pop("wall_s", None)
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # --dist-backend gloo --share-gpu: several ranks on one GPU (a functional check of
+    # the multi-rank path on a 1-GPU box; NCCL refuses duplicate GPUs)
+    local_dev = 0 if args.share_gpu else local
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(args.dist_backend)
     from paper_2505_24298_b200 import kernels as K
     from paper_2505_24298_b200.hotpath import DecoupledPPOStep, HotPathConfig, PackedRollouts
 
@@ -283,7 +289,7 @@ def run_ours(args, cfg):
     runner.k1_bytes = runner.k2_bytes = 0
     runner.record_events = True
     s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    with ClockSampler(local_dev) as clk:
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -386,6 +392,9 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-seconds", type=float, default=6.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--share-gpu", action="store_true",
+                    help="all ranks on cuda:0 (functional multi-rank check on one GPU)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)

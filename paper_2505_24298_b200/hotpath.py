@@ -245,7 +245,9 @@ class DecoupledPPOStep:
 
     # ---- K1 over this rank's micro-batches (prox, once per global batch)
     def prox_logprobs(self, ro: PackedRollouts, sp: StepPlan, logits_fn) -> torch.Tensor:
-        prox = torch.empty(ro.n_tokens, dtype=torch.float64, device=self.device)
+        # zeros: under DP each token's prox is written by exactly one rank, so a SUM
+        # all-reduce (if a caller needs the full vector) reconstructs it
+        prox = torch.zeros(ro.n_tokens, dtype=torch.float64, device=self.device)
         for m, groups in enumerate(sp.mine):
             for g, lo, hi in groups:
                 rows = sp.gather[lo:hi]
