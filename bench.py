@@ -47,6 +47,14 @@ CONFIGS = {
     "cfg3": dict(workload="Qwen2-7B shape (BASELINE configs[2])", vocab=152064, rollouts=1024,
                  prompts=256, len_lo=128, len_hi=27648, dtype="bf16", budget=32768,
                  minibatches=4, eta=4),
+    # configs[3]: GRPO group-normalised advantages, 16 samples/prompt, versions lag 0..8
+    "cfg4": dict(workload="GRPO 16 samples/prompt, mixed versions (BASELINE configs[3])",
+                 vocab=151936, rollouts=1024, prompts=64, len_lo=128, len_hi=8192, dtype="bf16",
+                 budget=32768, minibatches=4, eta=8, adv_norm="group"),
+    # configs[4]: heavy-tailed stress, reference Pareto sampler (timeline.py:84-90)
+    "cfg5": dict(workload="stress: 4096 rollouts, Pareto lengths 64-32768 (BASELINE configs[4])",
+                 vocab=151936, rollouts=4096, prompts=1024, pareto=(1.2, 64.0, 32768, 64),
+                 len_lo=64, len_hi=32768, dtype="bf16", budget=32768, minibatches=4),
 }
 
 
@@ -63,7 +71,12 @@ def workload_arrays(cfg, n_copies=1, seed=0):
     """Synthetic rollouts: lengths U[lo, hi], tokens uniform, rewards +-5, prompt groups."""
     rng = np.random.default_rng(seed)
     n = cfg["rollouts"] * n_copies
-    lengths = rng.integers(cfg["len_lo"], cfg["len_hi"] + 1, size=n)
+    if "pareto" in cfg:  # scale * (1 + pareto(alpha)) clipped to [1, cap], floored (timeline.py:84-90)
+        alpha, scale, cap, floor = cfg["pareto"]
+        draw = scale * (1.0 + rng.pareto(alpha, size=n))
+        lengths = np.maximum(np.minimum(np.maximum(draw, 1.0), cap).astype(np.int64), floor)
+    else:
+        lengths = rng.integers(cfg["len_lo"], cfg["len_hi"] + 1, size=n)
     bounds = np.concatenate([[0], np.cumsum(lengths)]).astype(np.int64)
     T = int(bounds[-1])
     tokens = rng.integers(0, cfg["vocab"], size=T, dtype=np.int64)
@@ -224,7 +237,8 @@ def run_ours(args, cfg):
     ldt = torch.bfloat16 if cfg["dtype"] == "bf16" else torch.float32
     C = cfg["budget"]
     hp = HotPathConfig(minibatches=cfg["minibatches"], micro_token_budget=C,
-                       micro_min_groups=max(1, world), eta_mask=cfg.get("eta", -1) if "eta" in cfg else -1)
+                       micro_min_groups=max(1, world), eta_mask=cfg.get("eta", -1),
+                       adv_norm=cfg.get("adv_norm", "global"))
     runner = DecoupledPPOStep(hp, dev)
 
     # synthetic model outputs: rotating logits buffers (> L2) + one dlogits buffer
@@ -255,7 +269,8 @@ def run_ours(args, cfg):
     pin = lambda a: torch.from_numpy(a).pin_memory()
     host = dict(traj_bounds=pin(W["bounds"]), tokens=pin(W["tokens"]),
                 behav=pin(np.zeros(W["T"])), rewards=pin(W["rewards"]),
-                versions=pin(W["versions"]) if "eta" in cfg else None)
+                versions=pin(W["versions"]) if "eta" in cfg else None,
+                group_ids=pin(W["group_ids"]) if cfg.get("adv_norm") == "group" else None)
     ro = PackedRollouts.from_host(**host, device=dev)
     torch.cuda.synchronize()
 
@@ -312,6 +327,7 @@ def run_ours(args, cfg):
     e2e_steps = max(1, args.e2e_steps)
     res_host = torch.empty((cfg["minibatches"], 8), dtype=torch.float64).pin_memory()
     s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    step(PackedRollouts.from_host(**host, device=dev))  # untimed e2e warm-up
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -387,7 +403,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--logit-buffers", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-seconds", type=float, default=6.0)

@@ -16,6 +16,7 @@
 //              vocab) exchange their partials through DSMEM, pass 2 rewrites each
 //              chunk in place as dlogits and streams it out with a bulk store.
 //              HBM traffic = one logits read + one dlogits write per element.
+#include <cstdlib>
 #include <type_traits>
 
 #include "common.cuh"
@@ -43,6 +44,7 @@ struct PpoArgs {
   int decoupled, eta_mask, cur_version;
   // ring kernel geometry
   int cluster_size;
+  int poly_vecs;           // pass-2 vectors per thread per chunk whose exp2 runs on the FMA pipe
   int64_t slice16;         // 16-byte units per cluster rank
   int nslots;
 };
@@ -716,12 +718,22 @@ __device__ __forceinline__ void row_ring_body(const PpoArgs& a) {
                   const float2 L2 = make_float2(Lim<float>::kLog2e, Lim<float>::kLog2e);
                   const float2 M2 = make_float2(-lse_s, -lse_s);
                   const float2 G2 = make_float2(g, g);
+                  if (sizeof(T) == 2 && j < a.poly_vecs) {  // MUFU offload (16-bit outputs)
 #pragma unroll
-                  for (int e = 0; e < E; e += 2) {
-                    const float2 t = ffma2(make_float2(f[e], f[e + 1]), L2, M2);
-                    const float2 d = fmul2(make_float2(fast_exp2(t.x), fast_exp2(t.y)), G2);
-                    f[e] = d.x;
-                    f[e + 1] = d.y;
+                    for (int e = 0; e < E; e += 2) {
+                      const float2 t = ffma2(make_float2(f[e], f[e + 1]), L2, M2);
+                      const float2 d = fmul2(exp2_poly3(t), G2);
+                      f[e] = d.x;
+                      f[e + 1] = d.y;
+                    }
+                  } else {
+#pragma unroll
+                    for (int e = 0; e < E; e += 2) {
+                      const float2 t = ffma2(make_float2(f[e], f[e + 1]), L2, M2);
+                      const float2 d = fmul2(make_float2(fast_exp2(t.x), fast_exp2(t.y)), G2);
+                      f[e] = d.x;
+                      f[e + 1] = d.y;
+                    }
                   }
                 } else {
 #pragma unroll
@@ -850,6 +862,15 @@ static int launch_ring(PpoArgs a, cudaStream_t stream, int cs_force) {
   }
   if ((V16 + CS - 1) / CS * 16 > (int64_t)0x7fffffff) return AREAL_ERR_UNSUPPORTED;
   a.cluster_size = CS;
+  {
+    // tuning knob: AREAL_POLY_VECS in [0, kVecPerThread] (default 0 = all exps on MUFU)
+    static const int poly = [] {
+      const char* s = getenv("AREAL_POLY_VECS");
+      const int v = s ? atoi(s) : 0;
+      return v < 0 ? 0 : (v > kVecPerThread ? kVecPerThread : v);
+    }();
+    a.poly_vecs = poly;
+  }
   a.slice16 = (V16 + CS - 1) / CS;
   a.nslots = nslots;
   const size_t smem = ring_smem_bytes(nslots);
