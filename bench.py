@@ -317,7 +317,7 @@ def run_ours(args, cfg):
             dist.barrier()
     runner.record_events = False
     ms = s_ev.elapsed_time(e_ev) / args.steps
-    launches = runner.launches // args.steps
+    launches = runner.launches  # all K steps of the timed region
     k2_ms = sum(s.elapsed_time(e) for s, e in runner.k2_events)
     k1_ms = sum(s.elapsed_time(e) for s, e in runner.k1_events)
     k2_bytes, k1_bytes = runner.k2_bytes, runner.k1_bytes
@@ -386,6 +386,7 @@ def run_ours(args, cfg):
                      note="public API DecoupledPPOStep.run from pinned host rollouts; "
                           "logits are device-resident model outputs"),
             gpu_launches=launches,
+            gpu_launches_per_step=launches // args.steps,
             clocks=clk.summary(),
             cpu_baseline=cpu_base,
             loss=res.loss, clip_fraction=res.clip_fraction,

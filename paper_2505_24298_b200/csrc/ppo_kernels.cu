@@ -57,17 +57,10 @@ struct TokenTerms {
   bool valid, clipped, masked;
 };
 
-__device__ __forceinline__ TokenTerms ppo_token(double lp, double behav, double prox, double adv,
-                                                int version, const PpoArgs& a) {
+// Given scale = exp(prox - behav) (1 for naive) and ratio = exp(lp - prox|behav).
+__device__ __forceinline__ TokenTerms ppo_token_terms(double scale, double ratio, double adv,
+                                                      int version, const PpoArgs& a) {
   TokenTerms t;
-  double scale, ratio;
-  if (a.decoupled) {
-    scale = exp(__dsub_rn(prox, behav));  // trainer.py:166
-    ratio = exp(__dsub_rn(lp, prox));     // trainer.py:167
-  } else {
-    scale = 1.0;                          // trainer.py:169
-    ratio = exp(__dsub_rn(lp, behav));    // trainer.py:170
-  }
   const bool valid = isfinite(scale) && isfinite(ratio);  // trainer.py:172
   bool masked = false;
   if (a.eta_mask >= 0 && (a.cur_version - version) > a.eta_mask) masked = true;
@@ -85,6 +78,13 @@ __device__ __forceinline__ TokenTerms ppo_token(double lp, double behav, double 
   t.valid = v;
   t.masked = masked;
   return t;
+}
+
+__device__ __forceinline__ TokenTerms ppo_token(double lp, double behav, double prox, double adv,
+                                                int version, const PpoArgs& a) {
+  if (a.decoupled)  // trainer.py:166-167
+    return ppo_token_terms(exp(__dsub_rn(prox, behav)), exp(__dsub_rn(lp, prox)), adv, version, a);
+  return ppo_token_terms(1.0, exp(__dsub_rn(lp, behav)), adv, version, a);  // trainer.py:169-170
 }
 
 __device__ __forceinline__ void stats_add(double st[AREAL_N_STATS], const TokenTerms& t,
@@ -324,475 +324,11 @@ __device__ __forceinline__ void row_warp_body(const PpoArgs& a) {
   }
 }
 
-// ================================================================== row_ring kernel
-constexpr int kChunkBytes = 32768;
-constexpr int kConsumerWarps = 16;
-constexpr int kConsumers = kConsumerWarps * 32;
-constexpr int kRingThreads = kConsumers + 32;  // + 1 producer warp
-constexpr int kBarConsumers = 1;                // named barrier id among consumer warps
-constexpr int kVecPerThread = kChunkBytes / 16 / kConsumers;  // 16-byte vectors per thread per chunk
-constexpr int kWarpBytes = kChunkBytes / kConsumerWarps;      // contiguous bytes a warp owns per chunk
+}  // namespace areal
 
-struct RingBcast {
-  double gc;                // grad_scale * coef
-  double lse;               // lse in shift units
-  long long tok;            // token id
-  unsigned long long dtok;  // dlogit of the token element (T bits)
-};
+#include "ppo_ring.cuh"
 
-struct RingSmemTail {
-  uint64_t xbar[2];                 // DSMEM exchange barriers (double-buffered by row parity)
-  uint64_t bcbar[2];                // epilogue -> consumers (double-buffered by row parity)
-  double xval[2][8][3];             // [parity][rank][m, s, sx]
-  float redf[2][kConsumerWarps][3]; // per-warp partials, double-buffered by row parity
-  double redd[2][kConsumerWarps][3];
-  RingBcast bc[2];
-  double st[AREAL_N_STATS];         // thread 0's running statistics
-  // cp.async prefetch targets (thread 0): token id one row ahead, then the row's
-  // token logit word and per-token scalars, so no register waits on global loads
-  long long pf_tok;
-  unsigned long long pf_xa;         // 4- or 8-byte aligned word holding x[token]
-  double pf_behav, pf_prox, pf_adv;
-  int pf_ver;
-};
-
-template <typename A> __device__ __forceinline__ A* red_ptr(RingSmemTail* t, int par);
-template <> __device__ __forceinline__ float* red_ptr<float>(RingSmemTail* t, int par) {
-  return &t->redf[par][0][0];
-}
-template <> __device__ __forceinline__ double* red_ptr<double>(RingSmemTail* t, int par) {
-  return &t->redd[par][0][0];
-}
-
-// Ring cursor: slot index and mbarrier phase parity, advanced without division.
-struct Cursor {
-  uint32_t slot, phase;
-  __device__ __forceinline__ void next(uint32_t nslots) {
-    if (++slot == nslots) {
-      slot = 0;
-      phase ^= 1u;
-    }
-  }
-};
-
-// Vector j (< kVecPerThread) of this thread inside a chunk: each warp owns a
-// contiguous kWarpBytes region, lanes read consecutive 16-byte vectors.
-__device__ __forceinline__ int vec_index(int warp, int lane, int j) {
-  return warp * (kWarpBytes / 16) + j * 32 + lane;
-}
-
-// Load this thread's vectors of a chunk (nvec valid vectors) as accumulation values.
-template <typename T>
-__device__ __forceinline__ void load_values(const uint4* q, int warp, int lane, int nvec,
-                                            typename Traits<T>::Acc* f) {
-  using A = typename Traits<T>::Acc;
-  constexpr int E = Vec<T>::N;
-  if (nvec == kChunkBytes / 16) {  // full chunk: branch-free
-#pragma unroll
-    for (int j = 0; j < kVecPerThread; ++j) {
-      A g[E];
-      Vec<T>::unpack(q[vec_index(warp, lane, j)], g);
-#pragma unroll
-      for (int e = 0; e < E; ++e) f[j * E + e] = g[e];
-    }
-  } else {
-#pragma unroll
-    for (int j = 0; j < kVecPerThread; ++j) {
-      const int vi = vec_index(warp, lane, j);
-      A g[E];
-      if (vi < nvec) {
-        Vec<T>::unpack(q[vi], g);
-      } else {
-#pragma unroll
-        for (int e = 0; e < E; ++e) g[e] = Lim<A>::ninf();
-      }
-#pragma unroll
-      for (int e = 0; e < E; ++e) f[j * E + e] = g[e];
-    }
-  }
-}
-
-// Fold this thread's values of one chunk into its running (m, s, sx).
-// fp32: packed f32x2 FFMA2/FADD2 around the MUFU ex2; fp64: scalar libdevice exp.
-template <typename T, bool ENT>
-__device__ __forceinline__ void fold_values(RowStat<typename Traits<T>::Acc>& rs,
-                                            const typename Traits<T>::Acc* f) {
-  using A = typename Traits<T>::Acc;
-  constexpr int N = kVecPerThread * Vec<T>::N;
-  A lmax = f[0];
-#pragma unroll
-  for (int i = 1; i < N; ++i) lmax = fmax(lmax, f[i]);
-  const A mn = fmax(rs.m, lmax);
-  const A muse = (mn == Lim<A>::ninf()) ? A(0) : mn;
-  const A c = Ex<A>::shift(muse);
-  const A r = Ex<A>::e(rs.m, c);  // rescale of the running sums (0 while m = -inf)
-  if constexpr (std::is_same<A, float>::value) {
-    const float2 L2 = make_float2(Lim<float>::kLog2e, Lim<float>::kLog2e);
-    const float2 C2 = make_float2(-c, -c);
-    float2 s2 = make_float2(0.f, 0.f), x2 = make_float2(0.f, 0.f);
-#pragma unroll
-    for (int i = 0; i < N; i += 2) {
-      const float2 v = make_float2(f[i], f[i + 1]);
-      const float2 t = ffma2(v, L2, C2);
-      const float2 e = make_float2(fast_exp2(t.x), fast_exp2(t.y));
-      s2 = fadd2(s2, e);
-      if (ENT) {  // p log p := 0 at p = 0
-        const float2 vc = make_float2(fmaxf(v.x, Lim<float>::lowest()), fmaxf(v.y, Lim<float>::lowest()));
-        x2 = ffma2(e, vc, x2);
-      }
-    }
-    rs.s = rs.s * r + (s2.x + s2.y);
-    if (ENT) rs.sx = rs.sx * r + (x2.x + x2.y);
-  } else {
-    A s0 = A(0), x0 = A(0);
-#pragma unroll
-    for (int i = 0; i < N; ++i) {
-      const A e = Ex<A>::e(f[i], c);
-      s0 += e;
-      if (ENT) x0 += e * fmax(f[i], Lim<A>::lowest());
-    }
-    rs.s = rs.s * r + s0;
-    if (ENT) rs.sx = rs.sx * r + x0;
-  }
-  rs.m = mn;
-}
-
-template <typename T> __device__ __forceinline__ unsigned long long to_bits(T v) {
-  unsigned long long b = 0;
-  memcpy(&b, &v, sizeof(T));
-  return b;
-}
-template <typename T> __device__ __forceinline__ T from_bits(unsigned long long b) {
-  T v;
-  memcpy(&v, &b, sizeof(T));
-  return v;
-}
-
-template <typename T, bool BWD, bool ENT>
-__device__ __forceinline__ void row_ring_body(const PpoArgs& a) {
-  using A = typename Traits<T>::Acc;
-  constexpr int E = Vec<T>::N;                 // elements per 16 bytes
-  constexpr int NV = kVecPerThread * E;        // values per thread per chunk
-  extern __shared__ __align__(1024) unsigned char smem[];
-  const uint32_t nslots = (uint32_t)a.nslots;
-  unsigned char* ring = smem;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)nslots * kChunkBytes);
-  uint64_t* empty = full + nslots;
-  RingSmemTail* tail = reinterpret_cast<RingSmemTail*>(empty + nslots);
-
-  const int CS = a.cluster_size;
-  const uint32_t rank = CS > 1 ? cluster_ctarank() : 0u;
-  const int64_t cid = CS > 1 ? (int64_t)cluster_id_x() : (int64_t)blockIdx.x;
-  const int64_t ncl = CS > 1 ? (int64_t)nclusters_x() : (int64_t)gridDim.x;
-  const int64_t V16 = (a.vocab * (int64_t)sizeof(T)) / 16;
-  const int64_t b16 = (int64_t)rank * a.slice16;
-  const int64_t e16 = min(V16, b16 + a.slice16);
-  const int slice_bytes = e16 > b16 ? (int)((e16 - b16) * 16) : 0;  // < 2^31 (checked on host)
-  const int nfull = slice_bytes / kChunkBytes;
-  const int last_bytes = slice_bytes - nfull * kChunkBytes;
-  const int nchunks = nfull + (last_bytes > 0 ? 1 : 0);
-  const int64_t slice_e0 = b16 * E;  // first vocab element of this rank's slice
-
-  if (threadIdx.x == 0) {
-    for (uint32_t s = 0; s < nslots; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kConsumerWarps);  // one arrive per consumer warp per use
-    }
-    mbar_init(&tail->xbar[0], CS);
-    mbar_init(&tail->xbar[1], CS);
-    mbar_init(&tail->bcbar[0], 1);
-    mbar_init(&tail->bcbar[1], 1);
-    fence_mbar_init_cluster();
-  }
-  __syncthreads();
-  if (CS > 1) cluster_sync_all();  // peers' exchange barriers initialised before any remote arrive
-
-  const int tid = threadIdx.x;
-  if (tid == 0) {
-    for (int j = 0; j < AREAL_N_STATS; ++j) tail->st[j] = 0.0;
-    if (cid < a.n_rows) {  // token id of the first row
-      const int64_t i0 = a.row_index ? (int64_t)a.row_index[cid] : cid;
-      cp_async8(&tail->pf_tok, a.tokens + i0);
-      cp_async_commit();
-    }
-  }
-
-  if (tid >= kConsumers) {
-    // ---------------- producer warp: one elected lane issues the TMA bulk loads
-    if (tid == kConsumers) {
-      Cursor cur = {0u, 0u};
-      uint32_t used = 0;  // slots filled at least once (no wait needed on first use)
-      for (int64_t row = cid; row < a.n_rows; row += ncl) {
-        const char* src = a.logits + row * a.ld_in_bytes + b16 * 16;
-        for (int c = 0; c < nchunks; ++c) {
-          if (used >= nslots) mbar_wait(&empty[cur.slot], cur.phase ^ 1u);
-          else ++used;
-          const uint32_t bytes = (uint32_t)(c < nfull ? kChunkBytes : last_bytes);
-          mbar_arrive_expect_tx(&full[cur.slot], bytes);
-          bulk_g2s(ring + (size_t)cur.slot * kChunkBytes, src + (size_t)c * kChunkBytes, bytes,
-                   &full[cur.slot]);
-          cur.next(nslots);
-        }
-      }
-    }
-  } else {
-    // ---------------- consumer warps
-    const int warp = tid >> 5, lane = tid & 31;
-    Cursor cur = {0u, 0u};     // ring position of the current row's chunk 0
-    Cursor pstart = cur;       // where pass 1 resumes (after the lookahead chunks)
-    int la = 0;                // chunks of the current row already folded by the lookahead
-    RowStat<A> carry;          // their partial statistics
-    carry.init();
-    bool pending = false;      // BWD, lane 0: last store's slot not yet released
-    uint32_t pend_slot = 0;
-    int64_t idx_cur = 0;       // thread 0: global token index of the current row
-    if (tid == 0 && cid < a.n_rows) idx_cur = a.row_index ? (int64_t)a.row_index[cid] : cid;
-    int it = 0;
-    for (int64_t row = cid; row < a.n_rows; row += ncl, ++it) {
-      const int par = it & 1;
-      const T* xrow = reinterpret_cast<const T*>(a.logits + row * a.ld_in_bytes);
-      const int64_t idx = idx_cur;  // thread 0 only (loaded a row ahead)
-      int32_t idx_next = 0;         // thread 0 only: row_index of the next row
-      if (tid == 0) {
-        // the token id was prefetched a row ahead; issue the row's scalar loads as
-        // cp.async into shared memory so their latency hides behind pass 1
-        if (row + ncl < a.n_rows) idx_next = a.row_index ? a.row_index[row + ncl] : (int32_t)(row + ncl);
-        cp_async_wait_all();
-        const int64_t tok = tail->pf_tok;
-        if (tok >= 0 && tok < a.vocab) {
-          const uintptr_t p = (uintptr_t)(xrow + tok);
-          if (sizeof(T) == 8) cp_async8(&tail->pf_xa, (const void*)p);
-          else cp_async4(&tail->pf_xa, (const void*)(p & ~(uintptr_t)3));
-        }
-        if (BWD) {
-          cp_async8(&tail->pf_behav, a.behav + idx);
-          if (a.prox) cp_async8(&tail->pf_prox, a.prox + idx);
-          cp_async8(&tail->pf_adv, a.adv + idx);
-          if (a.versions) cp_async4(&tail->pf_ver, a.versions + idx);
-        }
-        cp_async_commit();
-      }
-      // ---- pass 1: online (max, sum e, sum e*x) over the chunks as they land
-      RowStat<A> rs = carry;
-      Cursor cc = pstart;
-      for (int c = la; c < nchunks; ++c) {
-        mbar_wait(&full[cc.slot], cc.phase);
-        const int nvec = (c < nfull ? kChunkBytes : last_bytes) / 16;
-        const uint4* q = reinterpret_cast<const uint4*>(ring + (size_t)cc.slot * kChunkBytes);
-        A f[NV];
-        load_values<T>(q, warp, lane, nvec, f);
-        if (!BWD) {  // K1: the slot is free as soon as the values are in registers
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&empty[cc.slot]);
-        }
-        fold_values<T, ENT>(rs, f);
-        cc.next(nslots);
-      }
-      const Cursor after = cc;  // ring position of the next row's chunk 0
-      // ---- CTA reduce: warp shuffles, then warp 0 merges the warp partials (fixed order)
-      rs.warp_reduce();
-      A* red = red_ptr<A>(tail, par);
-      if (lane == 0) {
-        red[warp * 3 + 0] = rs.m;
-        red[warp * 3 + 1] = rs.s;
-        red[warp * 3 + 2] = rs.sx;
-      }
-      named_bar_sync(kBarConsumers, kConsumers);
-      if (warp == 0) {
-        RowStat<A> w;
-        if (lane < kConsumerWarps) {
-          w.m = red[lane * 3 + 0];
-          w.s = red[lane * 3 + 1];
-          w.sx = red[lane * 3 + 2];
-        } else {
-          w.init();
-        }
-        w.warp_reduce();
-        if (lane == 0) {
-          RowStat<A> tot = w;
-          if (CS > 1) {
-            // ---- cluster exchange through DSMEM: write my partial into every
-            // rank's slot [parity][my rank], release-arrive on its barrier.
-            for (int r = 0; r < CS; ++r) {
-              const uint32_t base = mapa_shared(smem_u32(&tail->xval[par][rank][0]), (uint32_t)r);
-              st_cluster_f64(base, (double)w.m);
-              st_cluster_f64(base + 8, (double)w.s);
-              st_cluster_f64(base + 16, (double)w.sx);
-              mbar_remote_arrive_release(mapa_shared(smem_u32(&tail->xbar[par]), (uint32_t)r));
-            }
-            mbar_wait_cluster(&tail->xbar[par], (it >> 1) & 1);
-            tot.init();
-            for (int r = 0; r < CS; ++r)
-              tot.merge((A)tail->xval[par][r][0], (A)tail->xval[par][r][1], (A)tail->xval[par][r][2]);
-          }
-          cp_async_wait_all();  // this row's token logit and scalars are in smem
-          const int64_t tok = tail->pf_tok;
-          double xa = __longlong_as_double(0x7ff8000000000000ll);  // invalid token -> NaN, excluded
-          if (tok >= 0 && tok < a.vocab) {
-            if (sizeof(T) == 8) {
-              xa = __longlong_as_double((long long)tail->pf_xa);
-            } else if (sizeof(T) == 4) {
-              xa = (double)__uint_as_float((uint32_t)tail->pf_xa);
-            } else {
-              const uint32_t w = (uint32_t)tail->pf_xa;
-              const unsigned short h = (unsigned short)((((uintptr_t)(xrow + tok)) & 2) ? (w >> 16) : (w & 0xffff));
-              xa = (double)Traits<T>::to_acc(from_bits<T>(h));
-            }
-          }
-          if (row + ncl < a.n_rows) {  // prefetch the next row's token id
-            cp_async8(&tail->pf_tok, a.tokens + idx_next);
-            cp_async_commit();
-          }
-          const A lse_s = Ex<A>::lse_shift(tot.m == Lim<A>::ninf() ? A(0) : tot.m, tot.s);
-          const double lse = Ex<A>::lse_nat(lse_s);
-          const double ent = ENT ? lse - (double)(tot.sx / tot.s) : 0.0;
-          const double lp = xa - lse;
-          if (rank == 0) {
-            if (a.lp_out) a.lp_out[idx] = lp;
-            if (ENT && a.ent_out) a.ent_out[idx] = ent;
-          }
-          if (BWD) {
-            const TokenTerms t = ppo_token(lp, tail->pf_behav, a.prox ? tail->pf_prox : 0.0,
-                                           tail->pf_adv, a.versions ? tail->pf_ver : 0, a);
-            if (rank == 0) stats_add(tail->st, t, ent);
-            const double gc = a.grad_scale * t.coef;
-            RingBcast& b = tail->bc[par];
-            b.gc = gc;
-            b.lse = (double)lse_s;
-            b.tok = tok;
-            // the token's own element: g * (p - 1), from the exact lp
-            b.dtok = to_bits<T>(Traits<T>::from_acc((A)(gc * (exp(lp) - 1.0))));
-            mbar_arrive(&tail->bcbar[par]);  // release: publishes bc[par]
-          }
-        }
-      }
-      if (BWD) {
-        // ---- lookahead: while warp 0 finishes the epilogue, fold the next row's
-        // chunks that already sit in the spare slots
-        const bool has_next = row + ncl < a.n_rows;
-        const int la_next = has_next ? min((int)nslots - nchunks, nchunks) : 0;
-        RowStat<A> nxt;
-        nxt.init();
-        Cursor lc = after;
-        for (int c = 0; c < la_next; ++c) {
-          mbar_wait(&full[lc.slot], lc.phase);
-          const int nvec = (c < nfull ? kChunkBytes : last_bytes) / 16;
-          const uint4* q = reinterpret_cast<const uint4*>(ring + (size_t)lc.slot * kChunkBytes);
-          A f[NV];
-          load_values<T>(q, warp, lane, nvec, f);
-          fold_values<T, ENT>(nxt, f);
-          lc.next(nslots);
-        }
-        carry = nxt;
-        la = la_next;
-        pstart = lc;
-
-        mbar_wait(&tail->bcbar[par], (it >> 1) & 1);
-        const RingBcast b = tail->bc[par];
-        const A g = (A)b.gc;
-        const A lse_s = (A)b.lse;
-        const int64_t tok_local = b.tok - slice_e0;  // may lie outside this slice
-        const T dtok = from_bits<T>(b.dtok);
-        char* drow = a.dlogits + row * a.ld_out_bytes + b16 * 16;
-        // ---- pass 2: dlogits = g * (softmax - onehot) in place; each warp stores
-        // its own contiguous part of the chunk and recycles the slot itself.
-        Cursor c2 = cur;
-        for (int c = 0; c < nchunks; ++c) {
-          const int cbytes = c < nfull ? kChunkBytes : last_bytes;
-          const int nvec = cbytes / 16;
-          uint4* q = reinterpret_cast<uint4*>(ring + (size_t)c2.slot * kChunkBytes);
-          if (g == A(0)) {  // no gradient through this token: zeros, no exponentials
-#pragma unroll
-            for (int j = 0; j < kVecPerThread; ++j) {
-              const int vi = vec_index(warp, lane, j);
-              if (vi < nvec) q[vi] = make_uint4(0, 0, 0, 0);
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < kVecPerThread; ++j) {
-              const int vi = vec_index(warp, lane, j);
-              if (nvec == kChunkBytes / 16 || vi < nvec) {
-                A f[E];
-                Vec<T>::unpack(q[vi], f);
-                if constexpr (std::is_same<A, float>::value) {
-                  const float2 L2 = make_float2(Lim<float>::kLog2e, Lim<float>::kLog2e);
-                  const float2 M2 = make_float2(-lse_s, -lse_s);
-                  const float2 G2 = make_float2(g, g);
-                  if (sizeof(T) == 2 && j < a.poly_vecs) {  // MUFU offload (16-bit outputs)
-#pragma unroll
-                    for (int e = 0; e < E; e += 2) {
-                      const float2 t = ffma2(make_float2(f[e], f[e + 1]), L2, M2);
-                      const float2 d = fmul2(exp2_poly3(t), G2);
-                      f[e] = d.x;
-                      f[e + 1] = d.y;
-                    }
-                  } else {
-#pragma unroll
-                    for (int e = 0; e < E; e += 2) {
-                      const float2 t = ffma2(make_float2(f[e], f[e + 1]), L2, M2);
-                      const float2 d = fmul2(make_float2(fast_exp2(t.x), fast_exp2(t.y)), G2);
-                      f[e] = d.x;
-                      f[e + 1] = d.y;
-                    }
-                  }
-                } else {
-#pragma unroll
-                  for (int e = 0; e < E; ++e) f[e] = g * exp(f[e] - lse_s);
-                }
-                q[vi] = Vec<T>::pack(f);
-              }
-            }
-            // the one-hot element: written by the thread that owns it
-            const int64_t toff = tok_local - (int64_t)c * (kChunkBytes / (int)sizeof(T));
-            if (toff >= 0 && toff < (int64_t)(cbytes / (int)sizeof(T))) {
-              const int tv = (int)(toff / E);
-              if (tv / (kWarpBytes / 16) == warp && (tv % 32) == lane)
-                reinterpret_cast<T*>(q)[toff] = dtok;
-            }
-          }
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            const int wb0 = warp * kWarpBytes;
-            if (wb0 < cbytes) {
-              bulk_s2g(drow + (size_t)c * kChunkBytes + wb0,
-                       ring + (size_t)c2.slot * kChunkBytes + wb0, (uint32_t)min(kWarpBytes, cbytes - wb0));
-            }
-            bulk_commit();
-            if (pending) {  // previous store has read its slot -> release it
-              bulk_wait_read<1>();
-              mbar_arrive(&empty[pend_slot]);
-            }
-            pending = true;
-            pend_slot = c2.slot;
-            if (c == nchunks - 1) {  // row end: drain so every slot of this row is free
-              bulk_wait_read<0>();   // before the next row's lookahead waits on them
-              mbar_arrive(&empty[pend_slot]);
-              pending = false;
-            }
-          }
-          c2.next(nslots);
-        }
-      } else {
-        pstart = after;
-      }
-      cur = after;
-      idx_cur = idx_next;
-    }
-    if (BWD && lane == 0) {
-      bulk_wait<0>();  // all dlogits stores complete before the CTA retires
-      if (pending) mbar_arrive(&empty[pend_slot]);
-    }
-  }
-  // all threads: final stats reduction (rank-0 CTAs carry the counters)
-  __syncthreads();
-  if (BWD) {
-    double cta[AREAL_N_STATS];
-    for (int j = 0; j < AREAL_N_STATS; ++j) cta[j] = tail->st[j];
-    finalize_stats(a, cta, kRingThreads);
-  }
-  if (CS > 1) cluster_sync_all();  // no CTA exits while a peer may still address its smem
-}
+namespace areal {
 
 // Distinct entry points per op so profiles name them: K1 = logprob_*, K2 = ppo_*.
 template <typename T>
