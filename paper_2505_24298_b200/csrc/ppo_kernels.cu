@@ -44,7 +44,6 @@ struct PpoArgs {
   int decoupled, eta_mask, cur_version;
   // ring kernel geometry
   int cluster_size;
-  int poly_vecs;           // pass-2 vectors per thread per chunk whose exp2 runs on the FMA pipe
   int64_t slice16;         // 16-byte units per cluster rank
   int nslots;
 };
@@ -395,18 +394,18 @@ static int launch_ring(PpoArgs a, cudaStream_t stream, int cs_force) {
     }
     if (CS < 0) return AREAL_ERR_UNSUPPORTED;
     if (cs_force > 0) CS = cs_force;
+    {
+      // tuning knob: AREAL_CLUSTER_SIZE in {2, 4, 8} forces a larger vocab split
+      static const int env_cs = [] {
+        const char* s = getenv("AREAL_CLUSTER_SIZE");
+        const int v = s ? atoi(s) : 0;
+        return (v == 2 || v == 4 || v == 8) ? v : 0;
+      }();
+      if (env_cs > CS) CS = env_cs;
+    }
   }
   if ((V16 + CS - 1) / CS * 16 > (int64_t)0x7fffffff) return AREAL_ERR_UNSUPPORTED;
   a.cluster_size = CS;
-  {
-    // tuning knob: AREAL_POLY_VECS in [0, kVecPerThread] (default 0 = all exps on MUFU)
-    static const int poly = [] {
-      const char* s = getenv("AREAL_POLY_VECS");
-      const int v = s ? atoi(s) : 0;
-      return v < 0 ? 0 : (v > kVecPerThread ? kVecPerThread : v);
-    }();
-    a.poly_vecs = poly;
-  }
   a.slice16 = (V16 + CS - 1) / CS;
   a.nslots = nslots;
   const size_t smem = ring_smem_bytes(nslots);

@@ -155,6 +155,27 @@ __device__ __forceinline__ void fold_values(RowStat<typename Traits<T>::Acc>& rs
   rs.m = mn;
 }
 
+// Merge the warp's per-lane partials into one (max, sum, sum*x), identical on every
+// lane: max-reduce, one rescale exp per lane, then two sum-reduces (XOR
+// butterflies, fixed order => deterministic and bitwise equal across lanes).
+template <typename A>
+__device__ __forceinline__ RowStat<A> warp_merge(const RowStat<A>& w) {
+  const A M = warp_max(w.m);
+  const A muse = (M == Lim<A>::ninf()) ? A(0) : M;
+  const A f = (w.m == Lim<A>::ninf()) ? A(0) : Ex<A>::e(w.m, Ex<A>::shift(muse));
+  A s = w.s * f, sx = w.sx * f;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    sx += __shfl_xor_sync(0xffffffffu, sx, o);
+  }
+  RowStat<A> r;
+  r.m = M;
+  r.s = s;
+  r.sx = sx;
+  return r;
+}
+
 template <typename T> __device__ __forceinline__ unsigned long long to_bits(T v) {
   unsigned long long b = 0;
   memcpy(&b, &v, sizeof(T));
@@ -257,7 +278,7 @@ __device__ __forceinline__ void row_ring_body(const PpoArgs& a) {
       } else {
         w.init();
       }
-      w.warp_reduce();  // every lane holds the CTA total
+      w = warp_merge(w);  // every lane holds the CTA total
       if (!BWD && lane == 0) mbar_arrive(&tail->bcbar[par]);  // K1: partials consumed
       RowStat<A> tot = w;
       if (CS > 1) {
@@ -280,7 +301,7 @@ __device__ __forceinline__ void row_ring_body(const PpoArgs& a) {
       const double ent = ENT ? lse - (double)(tot.sx / tot.s) : 0.0;
       xa = __shfl_sync(0xffffffffu, xa, 0);
       const double lp = xa - lse;
-      if (lane == 0 && rank == 0) {
+      if (!BWD && lane == 0 && rank == 0) {
         if (a.lp_out) a.lp_out[idx] = lp;
         if (ENT && a.ent_out) a.ent_out[idx] = ent;
       }
@@ -299,7 +320,6 @@ __device__ __forceinline__ void row_ring_body(const PpoArgs& a) {
         if (lane == 0) {
           const TokenTerms t = ppo_token_terms(a.decoupled ? e_scale : 1.0, e_ratio, sc_adv,
                                                sc_ver, a);
-          if (rank == 0) stats_add(tail->st, t, ent);
           const double gc = a.grad_scale * t.coef;
           RingBcast& b = tail->bc[par];
           b.gc = gc;
@@ -307,6 +327,12 @@ __device__ __forceinline__ void row_ring_body(const PpoArgs& a) {
           b.tok = tok;
           b.dtok = to_bits<T>(Traits<T>::from_acc((A)(gc * (e_p - 1.0))));  // g * (p_tok - 1)
           mbar_arrive(&tail->bcbar[par]);  // release: publishes bc[par]
+          // bookkeeping after the hand-off (off the math warps' critical path)
+          if (rank == 0) {
+            stats_add(tail->st, t, ent);
+            if (a.lp_out) a.lp_out[idx] = lp;
+            if (ENT && a.ent_out) a.ent_out[idx] = ent;
+          }
         }
       }
     }
@@ -402,22 +428,12 @@ __device__ __forceinline__ void row_ring_body(const PpoArgs& a) {
                   const float2 L2 = make_float2(Lim<float>::kLog2e, Lim<float>::kLog2e);
                   const float2 M2 = make_float2(-lse_s, -lse_s);
                   const float2 G2 = make_float2(g, g);
-                  if (sizeof(T) == 2 && j < a.poly_vecs) {  // MUFU offload (16-bit outputs)
 #pragma unroll
-                    for (int e = 0; e < E; e += 2) {
-                      const float2 t = ffma2(make_float2(f[e], f[e + 1]), L2, M2);
-                      const float2 d = fmul2(exp2_poly3(t), G2);
-                      f[e] = d.x;
-                      f[e + 1] = d.y;
-                    }
-                  } else {
-#pragma unroll
-                    for (int e = 0; e < E; e += 2) {
-                      const float2 t = ffma2(make_float2(f[e], f[e + 1]), L2, M2);
-                      const float2 d = fmul2(make_float2(fast_exp2(t.x), fast_exp2(t.y)), G2);
-                      f[e] = d.x;
-                      f[e + 1] = d.y;
-                    }
+                  for (int e = 0; e < E; e += 2) {
+                    const float2 t = ffma2(make_float2(f[e], f[e + 1]), L2, M2);
+                    const float2 d = fmul2(make_float2(fast_exp2(t.x), fast_exp2(t.y)), G2);
+                    f[e] = d.x;
+                    f[e + 1] = d.y;
                   }
                 } else {
 #pragma unroll

@@ -146,32 +146,6 @@ def test_ppo_masks_and_scale(algo):
     check_k2("f32", dl, st, ref, T)
 
 
-def test_ppo_poly_exp_offload_bf16(tmp_path):
-    """AREAL_POLY_VECS moves part of pass 2's exp2 to the FMA pipe (16-bit logits only)."""
-    import os
-    import subprocess
-    import sys
-    T, V = 96, 151936
-    logits, x64, tokens, behav, prox, adv = make_case(T, V, "bf16", seed=33)
-    np.savez(tmp_path / "in.npz", logits=logits.view(torch.int16).numpy(), tokens=tokens,
-             behav=behav, prox=prox, adv=adv)
-    code = f"""
-import numpy as np, torch, sys
-sys.path.insert(0, {repr(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))})
-from paper_2505_24298_b200 import kernels as K
-z = np.load({repr(str(tmp_path / 'in.npz'))})
-lg = torch.from_numpy(z['logits']).view(torch.bfloat16).cuda()
-c = lambda k: torch.from_numpy(z[k]).cuda()
-dl, st = K.ppo_fwd_bwd(lg, c('tokens'), c('behav'), c('prox'), c('adv'), algo='ring')
-np.savez({repr(str(tmp_path / 'out.npz'))}, dl=dl.double().cpu().numpy(), st=st.cpu().numpy())
-"""
-    env = dict(os.environ, AREAL_POLY_VECS="2")
-    subprocess.run([sys.executable, "-c", code], env=env, check=True, timeout=300)
-    out = np.load(tmp_path / "out.npz")
-    ref = O.surrogate_terms(x64, tokens, behav, prox, adv)
-    check_k2("bf16", out["dl"], out["st"], ref, T)
-
-
 @pytest.mark.parametrize("algo", ["warp", "ring"])
 def test_ppo_inplace_and_row_index(algo):
     T, V = 64, 32000
