@@ -326,8 +326,14 @@ __device__ __forceinline__ void row_warp_body(const PpoArgs& a) {
 }  // namespace areal
 
 #include "ppo_ring.cuh"
+#include "ppo_tmem.cuh"
 
 namespace areal {
+
+template <typename T, bool ENT>
+__global__ void __launch_bounds__(kRingThreads, 1) ppo_tmem_kernel(PpoArgs a) {
+  if constexpr (sizeof(T) == 2 || sizeof(T) == 4) tmem_k2_body<T, ENT>(a);
+}
 
 // Distinct entry points per op so profiles name them: K1 = logprob_*, K2 = ppo_*.
 template <typename T>
@@ -374,6 +380,26 @@ static int max_slots(const DevInfo& d) {
   return n;
 }
 
+template <typename T, bool ENT>
+static int launch_tmem(PpoArgs a, cudaStream_t stream, const DevInfo& d, int nslots) {
+  a.cluster_size = 1;
+  a.slice16 = (a.vocab * (int64_t)sizeof(T)) / 16;
+  a.nslots = nslots;
+  const size_t smem = ring_smem_bytes(nslots);
+  auto kern = ppo_tmem_kernel<T, ENT>;
+  static thread_local int attr_set[16] = {0};
+  const int dev = d.dev & 15;
+  if (!attr_set[dev]) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return AREAL_ERR_CUDA;
+    attr_set[dev] = 1;
+  }
+  const int64_t grid = std::min<int64_t>(a.n_rows, (int64_t)d.sms);  // one CTA (all of TMEM) per SM
+  kern<<<(unsigned)grid, kRingThreads, smem, stream>>>(a);
+  AREAL_CUDA_CHECK_LAUNCH();
+  return AREAL_OK;
+}
+
 template <typename T, bool BWD, bool ENT>
 static int launch_ring(PpoArgs a, cudaStream_t stream, int cs_force) {
   DevInfo d = get_dev();
@@ -402,6 +428,17 @@ static int launch_ring(PpoArgs a, cudaStream_t stream, int cs_force) {
         return (v == 2 || v == 4 || v == 8) ? v : 0;
       }();
       if (env_cs > CS) CS = env_cs;
+    }
+    // A row too long for one CTA's shared memory but within shared memory + TMEM
+    // runs on the single-CTA TMEM kernel (no cluster split) unless disabled.
+    if constexpr (sizeof(T) == 2 || sizeof(T) == 4) {
+      static const bool tmem_off = [] {
+        const char* s = getenv("AREAL_K2_TMEM");
+        return s && atoi(s) == 0;
+      }();
+      const int64_t row_chunks = (V16 * 16 + kChunkBytes - 1) / kChunkBytes;
+      if (CS > 1 && cs_force == 0 && !tmem_off && row_chunks <= kTmemMaxChunks && nslots == 7)
+        return launch_tmem<T, ENT>(a, stream, d, nslots);
     }
   }
   if ((V16 + CS - 1) / CS * 16 > (int64_t)0x7fffffff) return AREAL_ERR_UNSUPPORTED;

@@ -1,0 +1,351 @@
+// ppo_tmem.cuh — K2 with the row kept in Tensor Memory: one CTA per row, no cluster.
+//
+// A bf16 row of 151,936 logits (297 KB) exceeds shared memory (227 KB) but fits
+// shared memory + TMEM (256 KB per SM).  This variant parks the first
+// kTmemChunks 32 KB chunks of each row in TMEM (tcgen05.st 32x32b, each math
+// warp its own 2 KB per chunk in its lane quarter) and keeps only the row's
+// tail chunks resident in the shared-memory ring, so:
+//   * no thread-block cluster, no DSMEM exchange, no cross-CTA skew in the
+//     per-row epilogue (the measured cost of the 2-CTA split is ~20% of K2);
+//   * up to nslots - R spare ring slots for the next row's lookahead.
+// Pass 2 reads TMEM chunks back with tcgen05.ld, resident chunks from shared
+// memory, and writes dlogits with coalesced 16-byte global stores.
+//
+// Ring-slot liveness (deadlock freedom): chunks are streamed in row order into
+// ring slots in order; a slot is reused nslots chunks later.  TMEM-bound chunks
+// free their slot right after the shared-memory load in pass 1; the lookahead
+// chunks of row i+1 (folded during row i's epilogue) are parked into TMEM at the
+// start of row i+1's pass 1; resident tail chunks (offset >= kTmemChunks) free
+// their slot in pass 2.  A resident chunk at row offset x is reused by stream
+// position x + nslots, which must not be needed before its row's pass 2 starts:
+// x + nslots > nchunks - 1 + la, i.e. la <= nslots + kTmemChunks - nchunks.
+#pragma once
+
+namespace areal {
+
+constexpr int kTmemChunks = 8;        // 8 x 32 KB = the whole 256 KB of TMEM
+constexpr int kTmemCols = 512;
+constexpr int kTmemMaxChunks = 14;    // kTmemChunks + (nslots - 1) with 7 slots
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+      "r"(r[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+// TMEM address of math warp `warp`'s part of parked chunk t: lane quarter
+// (warp % 4) in bits 31:16, 16 columns per warp, 4 warps per quarter per chunk.
+__device__ __forceinline__ uint32_t tmem_addr(uint32_t base, int warp, int t) {
+  return base + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(t * 64 + (warp >> 2) * 16);
+}
+
+// Raw 16 words (4 x 16-byte vectors) of this thread's share of a chunk.
+__device__ __forceinline__ void lds_raw(const uint4* q, int warp, int lane, int nvec,
+                                        uint32_t (&w)[16]) {
+#pragma unroll
+  for (int j = 0; j < kVecPerThread; ++j) {
+    const int vi = vec_index(warp, lane, j);
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (nvec == kChunkBytes / 16 || vi < nvec) v = q[vi];
+    w[4 * j + 0] = v.x;
+    w[4 * j + 1] = v.y;
+    w[4 * j + 2] = v.z;
+    w[4 * j + 3] = v.w;
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void raw_to_values(const uint32_t (&w)[16], int warp, int lane, int nvec,
+                                              float* f) {
+  constexpr int E = Vec<T>::N;
+#pragma unroll
+  for (int j = 0; j < kVecPerThread; ++j) {
+    float g[E];
+    Vec<T>::unpack(make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]), g);
+    const bool ok = nvec == kChunkBytes / 16 || vec_index(warp, lane, j) < nvec;
+#pragma unroll
+    for (int e = 0; e < E; ++e) f[j * E + e] = ok ? g[e] : Lim<float>::ninf();
+  }
+}
+
+template <typename T, bool ENT>
+__device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
+  static_assert(sizeof(T) == 2 || sizeof(T) == 4, "TMEM K2 path: 16/32-bit logits");
+  using A = float;
+  constexpr int E = Vec<T>::N;
+  constexpr int NV = kVecPerThread * E;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  const uint32_t nslots = (uint32_t)a.nslots;
+  unsigned char* ring = smem;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)nslots * kChunkBytes);
+  uint64_t* empty = full + nslots;
+  RingSmemTail* tail = reinterpret_cast<RingSmemTail*>(empty + nslots);
+  __shared__ uint32_t s_tmem_base;
+
+  const int64_t row_bytes = a.vocab * (int64_t)sizeof(T);
+  const int nfull = (int)(row_bytes / kChunkBytes);
+  const int last_bytes = (int)(row_bytes - (int64_t)nfull * kChunkBytes);
+  const int nchunks = nfull + (last_bytes > 0 ? 1 : 0);
+  const int ntm = min(nchunks, kTmemChunks);     // chunks parked in TMEM
+  const int R = nchunks - ntm;                   // resident tail chunks
+  const int la_max = min(min((int)nslots - R, (int)nslots + kTmemChunks - nchunks), nchunks);
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (uint32_t s = 0; s < nslots; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
+    mbar_init(&tail->bcbar[0], 1);
+    mbar_init(&tail->bcbar[1], 1);
+    for (int j = 0; j < AREAL_N_STATS; ++j) tail->st[j] = 0.0;
+    fence_mbar_init_cluster();
+  }
+  if (warp == kEpilogueWarp) {  // one warp allocates (and later frees) all of TMEM
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&s_tmem_base)),
+                 "r"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    tmem_fence_before();
+  }
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t tbase = s_tmem_base;
+  const int64_t cid = blockIdx.x, ncl = gridDim.x;
+
+  if (warp == kProducerWarp) {
+    // ================= producer: TMA bulk loads of whole rows, chunk by chunk
+    if (lane == 0) {
+      Cursor cur = {0u, 0u};
+      uint32_t used = 0;
+      for (int64_t row = cid; row < a.n_rows; row += ncl) {
+        const char* src = a.logits + row * a.ld_in_bytes;
+        for (int c = 0; c < nchunks; ++c) {
+          if (used >= nslots) mbar_wait(&empty[cur.slot], cur.phase ^ 1u);
+          else ++used;
+          const uint32_t bytes = (uint32_t)(c < nfull ? kChunkBytes : last_bytes);
+          mbar_arrive_expect_tx(&full[cur.slot], bytes);
+          bulk_g2s(ring + (size_t)cur.slot * kChunkBytes, src + (size_t)c * kChunkBytes, bytes,
+                   &full[cur.slot]);
+          cur.next(nslots);
+        }
+      }
+    }
+  } else if (warp == kEpilogueWarp) {
+    // ================= epilogue: merge the 16 partials, fp64 per-token epilogue
+    int it = 0;
+    for (int64_t row = cid; row < a.n_rows; row += ncl, ++it) {
+      const int par = it & 1;
+      int64_t idx = 0, tok = -1;
+      double xa = 0.0, sc_behav = 0.0, sc_prox = 0.0, sc_adv = 0.0;
+      int sc_ver = 0;
+      if (lane == 0) {
+        idx = a.row_index ? (int64_t)a.row_index[row] : row;
+        tok = a.tokens[idx];
+        xa = token_logit<T>(a, reinterpret_cast<const T*>(a.logits + row * a.ld_in_bytes), tok);
+        sc_behav = a.behav[idx];
+        sc_prox = a.prox ? a.prox[idx] : 0.0;
+        sc_adv = a.adv[idx];
+        sc_ver = a.versions ? a.versions[idx] : 0;
+      }
+      named_bar_sync(kBarPartials, kBarPartialsThreads);
+      const A* red = red_ptr<A>(tail, par);
+      RowStat<A> w;
+      if (lane < kConsumerWarps) {
+        w.m = red[lane * 3 + 0];
+        w.s = red[lane * 3 + 1];
+        w.sx = red[lane * 3 + 2];
+      } else {
+        w.init();
+      }
+      const RowStat<A> tot = warp_merge(w);
+      const A lse_s = Ex<A>::lse_shift(tot.m == Lim<A>::ninf() ? A(0) : tot.m, tot.s);
+      const double lse = Ex<A>::lse_nat(lse_s);
+      const double ent = ENT ? lse - (double)(tot.sx / tot.s) : 0.0;
+      xa = __shfl_sync(0xffffffffu, xa, 0);
+      const double lp = xa - lse;
+      sc_behav = __shfl_sync(0xffffffffu, sc_behav, 0);
+      sc_prox = __shfl_sync(0xffffffffu, sc_prox, 0);
+      const double arg = lane == 0 ? __dsub_rn(sc_prox, sc_behav)
+                         : lane == 1 ? (a.decoupled ? __dsub_rn(lp, sc_prox) : __dsub_rn(lp, sc_behav))
+                                     : lp;
+      const double ex = exp(arg);
+      const double e_scale = __shfl_sync(0xffffffffu, ex, 0);
+      const double e_ratio = __shfl_sync(0xffffffffu, ex, 1);
+      const double e_p = __shfl_sync(0xffffffffu, ex, 2);
+      if (lane == 0) {
+        const TokenTerms t = ppo_token_terms(a.decoupled ? e_scale : 1.0, e_ratio, sc_adv, sc_ver, a);
+        const double gc = a.grad_scale * t.coef;
+        RingBcast& b = tail->bc[par];
+        b.gc = gc;
+        b.lse = (double)lse_s;
+        b.tok = tok;
+        b.dtok = to_bits<T>(Traits<T>::from_acc((A)(gc * (e_p - 1.0))));
+        mbar_arrive(&tail->bcbar[par]);
+        stats_add(tail->st, t, ent);
+        if (a.lp_out) a.lp_out[idx] = lp;
+        if (ENT && a.ent_out) a.ent_out[idx] = ent;
+      }
+    }
+  } else {
+    // ================= math warps
+    Cursor cur = {0u, 0u};  // ring position of the current row's chunk 0
+    int la = 0;             // chunks of the current row folded by the previous lookahead
+    RowStat<A> carry;
+    carry.init();
+    int it = 0;
+    for (int64_t row = cid; row < a.n_rows; row += ncl, ++it) {
+      const int par = it & 1;
+      // ---- park the lookahead chunks (already folded, still in their slots) in TMEM
+      Cursor cc = cur;
+      for (int c = 0; c < la; ++c) {
+        const int nvec = (c < nfull ? kChunkBytes : last_bytes) / 16;
+        uint32_t wv[16];
+        lds_raw(reinterpret_cast<const uint4*>(ring + (size_t)cc.slot * kChunkBytes), warp, lane,
+                nvec, wv);
+        tmem_st16(tmem_addr(tbase, warp, c), wv);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[cc.slot]);
+        cc.next(nslots);
+      }
+      // ---- pass 1 over the remaining chunks: TMEM-bound ones free their slot at once
+      RowStat<A> rs = carry;
+      for (int c = la; c < nchunks; ++c) {
+        mbar_wait(&full[cc.slot], cc.phase);
+        const int nvec = (c < nfull ? kChunkBytes : last_bytes) / 16;
+        uint32_t wv[16];
+        lds_raw(reinterpret_cast<const uint4*>(ring + (size_t)cc.slot * kChunkBytes), warp, lane,
+                nvec, wv);
+        if (c < ntm) {
+          tmem_st16(tmem_addr(tbase, warp, c), wv);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[cc.slot]);
+        }
+        A f[NV];
+        raw_to_values<T>(wv, warp, lane, nvec, f);
+        fold_values<T, ENT>(rs, f);
+        cc.next(nslots);
+      }
+      const Cursor after = cc;
+      tmem_wait_st();  // this row's parked chunks are in TMEM before pass 2 reads them
+      rs.warp_reduce();
+      A* red = red_ptr<A>(tail, par);
+      if (lane == 0) {
+        red[warp * 3 + 0] = rs.m;
+        red[warp * 3 + 1] = rs.s;
+        red[warp * 3 + 2] = rs.sx;
+      }
+      named_bar_arrive(kBarPartials, kBarPartialsThreads);
+      // ---- lookahead: fold the next row's first chunks while the epilogue runs
+      const bool has_next = row + ncl < a.n_rows;
+      const int la_next = has_next ? la_max : 0;
+      RowStat<A> nxt;
+      nxt.init();
+      Cursor lc = after;
+      for (int c = 0; c < la_next; ++c) {
+        mbar_wait(&full[lc.slot], lc.phase);
+        const int nvec = (c < nfull ? kChunkBytes : last_bytes) / 16;
+        A f[NV];
+        load_values<T>(reinterpret_cast<const uint4*>(ring + (size_t)lc.slot * kChunkBytes), warp,
+                       lane, nvec, f);
+        fold_values<T, ENT>(nxt, f);
+        lc.next(nslots);
+      }
+      carry = nxt;
+      la = la_next;
+
+      mbar_wait(&tail->bcbar[par], (it >> 1) & 1);
+      const RingBcast b = tail->bc[par];
+      const float g = (float)b.gc;
+      const float lse_s = (float)b.lse;
+      const T dtok = from_bits<T>(b.dtok);
+      char* drow = a.dlogits + row * a.ld_out_bytes;
+      // ---- pass 2: dlogits = g * softmax (one-hot element patched), 16-byte global stores
+      Cursor c2 = cur;
+      for (int c = 0; c < nchunks; ++c) {
+        const int cbytes = c < nfull ? kChunkBytes : last_bytes;
+        const int nvec = cbytes / 16;
+        uint32_t wv[16];
+        if (c < ntm) {
+          tmem_ld16(tmem_addr(tbase, warp, c), wv);
+          tmem_wait_ld();
+        } else {  // resident tail chunk (its full barrier completed in pass 1)
+          lds_raw(reinterpret_cast<const uint4*>(ring + (size_t)c2.slot * kChunkBytes), warp, lane,
+                  nvec, wv);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[c2.slot]);
+        }
+        const int64_t toff = b.tok - (int64_t)c * (kChunkBytes / (int)sizeof(T));
+        uint4* dst = reinterpret_cast<uint4*>(drow + (size_t)c * kChunkBytes);
+#pragma unroll
+        for (int j = 0; j < kVecPerThread; ++j) {
+          const int vi = vec_index(warp, lane, j);
+          if (nvec == kChunkBytes / 16 || vi < nvec) {
+            float f[E];
+            if (g == 0.f) {
+#pragma unroll
+              for (int e = 0; e < E; ++e) f[e] = 0.f;
+            } else {
+              Vec<T>::unpack(make_uint4(wv[4 * j], wv[4 * j + 1], wv[4 * j + 2], wv[4 * j + 3]), f);
+              const float2 L2 = make_float2(Lim<float>::kLog2e, Lim<float>::kLog2e);
+              const float2 M2 = make_float2(-lse_s, -lse_s);
+              const float2 G2 = make_float2(g, g);
+#pragma unroll
+              for (int e = 0; e < E; e += 2) {
+                const float2 t = ffma2(make_float2(f[e], f[e + 1]), L2, M2);
+                const float2 d = fmul2(make_float2(fast_exp2(t.x), fast_exp2(t.y)), G2);
+                f[e] = d.x;
+                f[e + 1] = d.y;
+              }
+            }
+            const int64_t eoff = toff - (int64_t)vi * E;
+            if (g != 0.f && eoff >= 0 && eoff < E) {  // the one-hot element (exact: a T value)
+#pragma unroll
+              for (int e = 0; e < E; ++e)
+                if (e == eoff) f[e] = Traits<T>::to_acc(dtok);
+            }
+            dst[vi] = Vec<T>::pack(f);
+          }
+        }
+        c2.next(nslots);
+      }
+      cur = after;
+    }
+    tmem_fence_before();
+  }
+  __syncthreads();
+  if (warp == kEpilogueWarp) {
+    tmem_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(kTmemCols)
+                 : "memory");
+  }
+  double cta[AREAL_N_STATS];
+  for (int j = 0; j < AREAL_N_STATS; ++j) cta[j] = tail->st[j];
+  finalize_stats(a, cta, kRingThreads);
+}
+
+}  // namespace areal
