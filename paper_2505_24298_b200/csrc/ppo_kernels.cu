@@ -380,12 +380,17 @@ static int max_slots(const DevInfo& d) {
   return n;
 }
 
+static size_t tmem_smem_bytes(int nslots) {
+  return (size_t)nslots * kChunkBytes + 2 * (size_t)nslots * sizeof(uint64_t) + sizeof(TmemTail);
+}
+
 template <typename T, bool ENT>
 static int launch_tmem(PpoArgs a, cudaStream_t stream, const DevInfo& d, int nslots) {
   a.cluster_size = 1;
   a.slice16 = (a.vocab * (int64_t)sizeof(T)) / 16;
   a.nslots = nslots;
-  const size_t smem = ring_smem_bytes(nslots);
+  const size_t smem = tmem_smem_bytes(nslots);
+  if (smem + 256 > (size_t)d.smem_optin) return AREAL_ERR_UNSUPPORTED;  // + static smem
   auto kern = ppo_tmem_kernel<T, ENT>;
   static thread_local int attr_set[16] = {0};
   const int dev = d.dev & 15;

@@ -192,7 +192,7 @@ __device__ __forceinline__ void row_ring_body(const PpoArgs& a) {
   using A = typename Traits<T>::Acc;
   constexpr int E = Vec<T>::N;                 // elements per 16 bytes
   constexpr int NV = kVecPerThread * E;        // values per thread per chunk
-  extern __shared__ __align__(1024) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];  // 1-D bulk copies need 16 B
   const uint32_t nslots = (uint32_t)a.nslots;
   unsigned char* ring = smem;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)nslots * kChunkBytes);

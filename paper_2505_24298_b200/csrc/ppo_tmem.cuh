@@ -8,15 +8,19 @@
 //   * no thread-block cluster, no DSMEM exchange, no cross-CTA skew in the
 //     per-row epilogue (the measured cost of the 2-CTA split is ~20% of K2);
 //   * up to nslots - R spare ring slots for the next row's lookahead.
-// Pass 2 reads TMEM chunks back with tcgen05.ld, resident chunks from shared
-// memory, and writes dlogits with coalesced 16-byte global stores.
+// Pass 1 computes e = 2^(x log2e - c) once per logit (c: warp-uniform running
+// max of the chunk) and parks e (bf16 bits for 16-bit logits, fp32 for fp32)
+// instead of x, so pass 2 is one multiply per logit: dlogit = e * g 2^(c - lse)
+// — half the MUFU work of recomputing the exponential.  Pass 2 reads TMEM with
+// tcgen05.ld, resident chunks from shared memory, and writes dlogits with
+// coalesced 16-byte global stores.
 //
 // Ring-slot liveness (deadlock freedom): chunks are streamed in row order into
 // ring slots in order; a slot is reused nslots chunks later.  TMEM-bound chunks
-// free their slot right after the shared-memory load in pass 1; the lookahead
-// chunks of row i+1 (folded during row i's epilogue) are parked into TMEM at the
-// start of row i+1's pass 1; resident tail chunks (offset >= kTmemChunks) free
-// their slot in pass 2.  A resident chunk at row offset x is reused by stream
+// free their slot right after pass 1 stores them to TMEM; the lookahead chunks
+// of row i+1 (folded during row i's epilogue) are parked into TMEM at the start
+// of row i+1's pass 1; resident tail chunks (offset >= kTmemChunks) free their
+// slot in pass 2.  A resident chunk at row offset x is reused by stream
 // position x + nslots, which must not be needed before its row's pass 2 starts:
 // x + nslots > nchunks - 1 + la, i.e. la <= nslots + kTmemChunks - nchunks.
 #pragma once
@@ -26,6 +30,14 @@ namespace areal {
 constexpr int kTmemChunks = 8;        // 8 x 32 KB = the whole 256 KB of TMEM
 constexpr int kTmemCols = 512;
 constexpr int kTmemMaxChunks = 14;    // kTmemChunks + (nslots - 1) with 7 slots
+
+struct TmemTail {
+  uint64_t bcbar[2];                          // epilogue -> math warps (row parity)
+  float red[2][kConsumerWarps][3];            // per-warp partials (row parity)
+  RingBcast bc[2];
+  double st[AREAL_N_STATS];
+  float cw[2][kTmemMaxChunks][kConsumerWarps];  // shift c of the stored e (row parity)
+};
 
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
   asm volatile(
@@ -61,7 +73,7 @@ __device__ __forceinline__ uint32_t tmem_addr(uint32_t base, int warp, int t) {
   return base + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(t * 64 + (warp >> 2) * 16);
 }
 
-// Raw 16 words (4 x 16-byte vectors) of this thread's share of a chunk.
+// This thread's share of a chunk as 16 raw 32-bit words (4 x 16-byte vectors).
 __device__ __forceinline__ void lds_raw(const uint4* q, int warp, int lane, int nvec,
                                         uint32_t (&w)[16]) {
 #pragma unroll
@@ -75,11 +87,31 @@ __device__ __forceinline__ void lds_raw(const uint4* q, int warp, int lane, int 
     w[4 * j + 3] = v.w;
   }
 }
+__device__ __forceinline__ void sts_raw(uint4* q, int warp, int lane, int nvec,
+                                        const uint32_t (&w)[16]) {
+#pragma unroll
+  for (int j = 0; j < kVecPerThread; ++j) {
+    const int vi = vec_index(warp, lane, j);
+    if (nvec == kChunkBytes / 16 || vi < nvec)
+      q[vi] = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+  }
+}
 
-template <typename T>
-__device__ __forceinline__ void raw_to_values(const uint32_t (&w)[16], int warp, int lane, int nvec,
-                                              float* f) {
+// Stored-e format: bf16 bits for 16-bit logits (e in [0, 1] keeps fp32's exponent
+// range), fp32 for fp32 logits.
+template <typename T> struct EFmt;
+template <> struct EFmt<__nv_bfloat16> { using V = Vec<__nv_bfloat16>; };
+template <> struct EFmt<__half> { using V = Vec<__nv_bfloat16>; };
+template <> struct EFmt<float> { using V = Vec<float>; };
+
+// Pass-1 fold of one chunk held as raw words: warp-uniform running max, e computed
+// once, the e words returned in place of the logits and the shift c returned.
+template <typename T, bool ENT>
+__device__ __forceinline__ float fold_to_e(RowStat<float>& rs, uint32_t (&w)[16], int warp, int lane,
+                                           int nvec) {
   constexpr int E = Vec<T>::N;
+  constexpr int N = kVecPerThread * E;
+  float f[N];
 #pragma unroll
   for (int j = 0; j < kVecPerThread; ++j) {
     float g[E];
@@ -88,6 +120,43 @@ __device__ __forceinline__ void raw_to_values(const uint32_t (&w)[16], int warp,
 #pragma unroll
     for (int e = 0; e < E; ++e) f[j * E + e] = ok ? g[e] : Lim<float>::ninf();
   }
+  float lmax = f[0];
+#pragma unroll
+  for (int i = 1; i < N; ++i) lmax = fmaxf(lmax, f[i]);
+  lmax = warp_max(lmax);
+  const float mn = fmaxf(rs.m, lmax);
+  const float muse = (mn == Lim<float>::ninf()) ? 0.f : mn;
+  const float c = Ex<float>::shift(muse);
+  const float r = Ex<float>::e(rs.m, c);
+  const float2 L2 = make_float2(Lim<float>::kLog2e, Lim<float>::kLog2e);
+  const float2 C2 = make_float2(-c, -c);
+  float2 s2 = make_float2(0.f, 0.f), x2 = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int j = 0; j < kVecPerThread; ++j) {
+    float ev[E];
+#pragma unroll
+    for (int k = 0; k < E; k += 2) {
+      const float2 v = make_float2(f[j * E + k], f[j * E + k + 1]);
+      const float2 t = ffma2(v, L2, C2);
+      const float2 ee = make_float2(fast_exp2(t.x), fast_exp2(t.y));
+      s2 = fadd2(s2, ee);
+      if (ENT) {  // p log p := 0 at p = 0
+        const float2 vc = make_float2(fmaxf(v.x, Lim<float>::lowest()), fmaxf(v.y, Lim<float>::lowest()));
+        x2 = ffma2(ee, vc, x2);
+      }
+      ev[k] = ee.x;
+      ev[k + 1] = ee.y;
+    }
+    const uint4 pk = EFmt<T>::V::pack(ev);
+    w[4 * j + 0] = pk.x;
+    w[4 * j + 1] = pk.y;
+    w[4 * j + 2] = pk.z;
+    w[4 * j + 3] = pk.w;
+  }
+  rs.s = rs.s * r + (s2.x + s2.y);
+  if (ENT) rs.sx = rs.sx * r + (x2.x + x2.y);
+  rs.m = mn;
+  return c;
 }
 
 template <typename T, bool ENT>
@@ -95,13 +164,12 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
   static_assert(sizeof(T) == 2 || sizeof(T) == 4, "TMEM K2 path: 16/32-bit logits");
   using A = float;
   constexpr int E = Vec<T>::N;
-  constexpr int NV = kVecPerThread * E;
-  extern __shared__ __align__(1024) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];  // 1-D bulk copies need 16 B
   const uint32_t nslots = (uint32_t)a.nslots;
   unsigned char* ring = smem;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)nslots * kChunkBytes);
   uint64_t* empty = full + nslots;
-  RingSmemTail* tail = reinterpret_cast<RingSmemTail*>(empty + nslots);
+  TmemTail* tail = reinterpret_cast<TmemTail*>(empty + nslots);
   __shared__ uint32_t s_tmem_base;
 
   const int64_t row_bytes = a.vocab * (int64_t)sizeof(T);
@@ -173,12 +241,11 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
         sc_ver = a.versions ? a.versions[idx] : 0;
       }
       named_bar_sync(kBarPartials, kBarPartialsThreads);
-      const A* red = red_ptr<A>(tail, par);
       RowStat<A> w;
       if (lane < kConsumerWarps) {
-        w.m = red[lane * 3 + 0];
-        w.s = red[lane * 3 + 1];
-        w.sx = red[lane * 3 + 2];
+        w.m = tail->red[par][lane][0];
+        w.s = tail->red[par][lane][1];
+        w.sx = tail->red[par][lane][2];
       } else {
         w.init();
       }
@@ -220,7 +287,8 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
     int it = 0;
     for (int64_t row = cid; row < a.n_rows; row += ncl, ++it) {
       const int par = it & 1;
-      // ---- park the lookahead chunks (already folded, still in their slots) in TMEM
+      float* cw = &tail->cw[par][0][0];  // [chunk][warp]
+      // ---- park the lookahead chunks (their e is in the ring slots) in TMEM
       Cursor cc = cur;
       for (int c = 0; c < la; ++c) {
         const int nvec = (c < nfull ? kChunkBytes : last_bytes) / 16;
@@ -232,47 +300,50 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
         if (lane == 0) mbar_arrive(&empty[cc.slot]);
         cc.next(nslots);
       }
-      // ---- pass 1 over the remaining chunks: TMEM-bound ones free their slot at once
+      // ---- pass 1 over the remaining chunks: e to TMEM (slot freed at once) or in place
       RowStat<A> rs = carry;
       for (int c = la; c < nchunks; ++c) {
         mbar_wait(&full[cc.slot], cc.phase);
         const int nvec = (c < nfull ? kChunkBytes : last_bytes) / 16;
+        uint4* q = reinterpret_cast<uint4*>(ring + (size_t)cc.slot * kChunkBytes);
         uint32_t wv[16];
-        lds_raw(reinterpret_cast<const uint4*>(ring + (size_t)cc.slot * kChunkBytes), warp, lane,
-                nvec, wv);
+        lds_raw(q, warp, lane, nvec, wv);
+        const float cshift = fold_to_e<T, ENT>(rs, wv, warp, lane, nvec);
+        if (lane == 0) cw[c * kConsumerWarps + warp] = cshift;
         if (c < ntm) {
           tmem_st16(tmem_addr(tbase, warp, c), wv);
           __syncwarp();
           if (lane == 0) mbar_arrive(&empty[cc.slot]);
+        } else {
+          sts_raw(q, warp, lane, nvec, wv);  // resident tail chunk: e in place
         }
-        A f[NV];
-        raw_to_values<T>(wv, warp, lane, nvec, f);
-        fold_values<T, ENT>(rs, f);
         cc.next(nslots);
       }
       const Cursor after = cc;
       tmem_wait_st();  // this row's parked chunks are in TMEM before pass 2 reads them
       rs.warp_reduce();
-      A* red = red_ptr<A>(tail, par);
       if (lane == 0) {
-        red[warp * 3 + 0] = rs.m;
-        red[warp * 3 + 1] = rs.s;
-        red[warp * 3 + 2] = rs.sx;
+        tail->red[par][warp][0] = rs.m;
+        tail->red[par][warp][1] = rs.s;
+        tail->red[par][warp][2] = rs.sx;
       }
       named_bar_arrive(kBarPartials, kBarPartialsThreads);
-      // ---- lookahead: fold the next row's first chunks while the epilogue runs
+      // ---- lookahead: fold the next row's first chunks (e in place) during the epilogue
       const bool has_next = row + ncl < a.n_rows;
       const int la_next = has_next ? la_max : 0;
+      float* cwn = &tail->cw[par ^ 1][0][0];
       RowStat<A> nxt;
       nxt.init();
       Cursor lc = after;
       for (int c = 0; c < la_next; ++c) {
         mbar_wait(&full[lc.slot], lc.phase);
         const int nvec = (c < nfull ? kChunkBytes : last_bytes) / 16;
-        A f[NV];
-        load_values<T>(reinterpret_cast<const uint4*>(ring + (size_t)lc.slot * kChunkBytes), warp,
-                       lane, nvec, f);
-        fold_values<T, ENT>(nxt, f);
+        uint4* q = reinterpret_cast<uint4*>(ring + (size_t)lc.slot * kChunkBytes);
+        uint32_t wv[16];
+        lds_raw(q, warp, lane, nvec, wv);
+        const float cshift = fold_to_e<T, ENT>(nxt, wv, warp, lane, nvec);
+        if (lane == 0) cwn[c * kConsumerWarps + warp] = cshift;
+        sts_raw(q, warp, lane, nvec, wv);
         lc.next(nslots);
       }
       carry = nxt;
@@ -284,21 +355,27 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
       const float lse_s = (float)b.lse;
       const T dtok = from_bits<T>(b.dtok);
       char* drow = a.dlogits + row * a.ld_out_bytes;
-      // ---- pass 2: dlogits = g * softmax (one-hot element patched), 16-byte global stores
+      // ---- pass 2: dlogits = e * g 2^(c - lse) (one-hot element patched), 16-byte stores
       Cursor c2 = cur;
       for (int c = 0; c < nchunks; ++c) {
         const int cbytes = c < nfull ? kChunkBytes : last_bytes;
         const int nvec = cbytes / 16;
         uint32_t wv[16];
-        if (c < ntm) {
-          tmem_ld16(tmem_addr(tbase, warp, c), wv);
-          tmem_wait_ld();
-        } else {  // resident tail chunk (its full barrier completed in pass 1)
-          lds_raw(reinterpret_cast<const uint4*>(ring + (size_t)c2.slot * kChunkBytes), warp, lane,
-                  nvec, wv);
+        if (g != 0.f) {
+          if (c < ntm) {
+            tmem_ld16(tmem_addr(tbase, warp, c), wv);
+            tmem_wait_ld();
+          } else {  // resident tail chunk (its full barrier completed in pass 1)
+            lds_raw(reinterpret_cast<const uint4*>(ring + (size_t)c2.slot * kChunkBytes), warp,
+                    lane, nvec, wv);
+          }
+        }
+        if (c >= ntm) {
           __syncwarp();
           if (lane == 0) mbar_arrive(&empty[c2.slot]);
         }
+        const float F = g * fast_exp2(cw[c * kConsumerWarps + warp] - lse_s);
+        const float2 F2 = make_float2(F, F);
         const int64_t toff = b.tok - (int64_t)c * (kChunkBytes / (int)sizeof(T));
         uint4* dst = reinterpret_cast<uint4*>(drow + (size_t)c * kChunkBytes);
 #pragma unroll
@@ -310,23 +387,19 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
 #pragma unroll
               for (int e = 0; e < E; ++e) f[e] = 0.f;
             } else {
-              Vec<T>::unpack(make_uint4(wv[4 * j], wv[4 * j + 1], wv[4 * j + 2], wv[4 * j + 3]), f);
-              const float2 L2 = make_float2(Lim<float>::kLog2e, Lim<float>::kLog2e);
-              const float2 M2 = make_float2(-lse_s, -lse_s);
-              const float2 G2 = make_float2(g, g);
+              EFmt<T>::V::unpack(make_uint4(wv[4 * j], wv[4 * j + 1], wv[4 * j + 2], wv[4 * j + 3]), f);
 #pragma unroll
               for (int e = 0; e < E; e += 2) {
-                const float2 t = ffma2(make_float2(f[e], f[e + 1]), L2, M2);
-                const float2 d = fmul2(make_float2(fast_exp2(t.x), fast_exp2(t.y)), G2);
+                const float2 d = fmul2(make_float2(f[e], f[e + 1]), F2);
                 f[e] = d.x;
                 f[e + 1] = d.y;
               }
-            }
-            const int64_t eoff = toff - (int64_t)vi * E;
-            if (g != 0.f && eoff >= 0 && eoff < E) {  // the one-hot element (exact: a T value)
+              const int64_t eoff = toff - (int64_t)vi * E;
+              if (eoff >= 0 && eoff < E) {  // the one-hot element (exact: a T value)
 #pragma unroll
-              for (int e = 0; e < E; ++e)
-                if (e == eoff) f[e] = Traits<T>::to_acc(dtok);
+                for (int e = 0; e < E; ++e)
+                  if (e == eoff) f[e] = Traits<T>::to_acc(dtok);
+              }
             }
             dst[vi] = Vec<T>::pack(f);
           }
