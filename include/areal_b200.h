@@ -176,6 +176,43 @@ int areal_fill_gather(const int64_t* traj_bounds, const int32_t* packed_traj,
                       const int64_t* seq_cu, int32_t n_items, int64_t n_packed_tokens,
                       int32_t* gather, int32_t* seq_id, void* stream);
 
+/* ---- K6: fused global-norm clip + Adam (decoupled weight decay), multi-tensor --
+ * Replaces the optimizer step of train_step (trainer.py:329-331): grad.scale_(-1/n)
+ * then apply_update (policy.py:225-258) with clip_by_global_norm (policy.py:215-221).
+ * For every tensor k (n_tensors <= AREAL_ADAM_MAX_TENSORS):
+ *   g = grad*grad_scale; norm = sqrt(sum_k sum(g_k**2)); if clip_norm > 0 and
+ *   norm > clip_norm: g *= clip_norm/norm; m = b1*m + (1-b1)*g; v = b2*v + (1-b2)*g*g;
+ *   p -= lr*((m/c1)/(sqrt(v/c2) + eps) + wd*p).
+ * The host passes the scalars the reference computes in Python ((1-b), c = 1-b**step,
+ * grad_scale = -1/n).  exact_norm = 1 (fp64 only) replays numpy's pairwise sums so the
+ * update is bit-identical to the reference for the same gradient.  If any scaled
+ * gradient is non-finite nothing is written and norm_out[1] (device, may be NULL;
+ * norm_out[0] = global norm) counts them: the caller raises NonFiniteGradientError
+ * (policy.py:234-239).  param/exp_avg/exp_avg_sq share param_dtype (F64 or F32);
+ * grads are F64 with F64 params, or F32/BF16/F16 with F32 master params.  No host
+ * synchronisation.  Uses the upper half of the workspace (like K3). */
+#define AREAL_ADAM_MAX_TENSORS 32
+
+typedef struct {
+  void* param;
+  const void* grad;
+  void* exp_avg;
+  void* exp_avg_sq;
+  int64_t numel;
+} areal_adam_tensor_t;
+
+typedef struct {
+  double lr, beta1, beta2, eps, weight_decay, clip_norm; /* AdamConfig (policy.py:188-196) */
+  double one_minus_beta1, one_minus_beta2;               /* 1 - beta, as Python computes it */
+  double bias_correction1, bias_correction2;             /* 1 - beta**step (policy.py:249-250) */
+  double grad_scale;                                     /* -1/n (trainer.py:330) or 1 */
+  int32_t exact_norm;                                    /* 1: numpy-exact fp64 norm */
+} areal_adam_params_t;
+
+int areal_adam_step(const areal_adam_tensor_t* tensors, int32_t n_tensors, int param_dtype,
+                    int grad_dtype, const areal_adam_params_t* params, double* norm_out,
+                    void* workspace, size_t workspace_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -26,7 +26,7 @@ __all__ = [
     "surrogate_terms", "STAT_NAMES", "compute_advantages_ref", "numpy_pairwise_sum",
     "gae_raw", "normalize_global", "normalize_group", "advantages",
     "allocate_microbatches", "minibatch_splits", "train_step_plan",
-    "AdamCfg", "linear_logits", "linear_train_step", "linear_loss",
+    "AdamCfg", "adam_update", "linear_logits", "linear_train_step", "linear_loss",
 ]
 
 
@@ -387,8 +387,9 @@ def linear_loss(features, tokens, behav, prox, adv, W, b, clip_eps=0.2, decouple
             "clip_fraction": s[2] / n, "mean_ratio": s[3] / n, "excluded": int(s[4])}
 
 
-def _adam(W, b, gw, gb, m_w, v_w, m_b, v_b, step, cfg: AdamCfg):
-    """apply_update restated (policy.py:225-258)."""
+def adam_update(W, b, gw, gb, m_w, v_w, m_b, v_b, step, cfg: AdamCfg):
+    """apply_update restated (policy.py:215-258): non-finite check, clip_by_global_norm,
+    Adam with decoupled weight decay; grads already scaled by -1/n (trainer.py:330)."""
     if not (np.all(np.isfinite(gw)) and np.all(np.isfinite(gb))):
         raise FloatingPointError("non-finite gradient")
     norm = math.sqrt(float(np.sum(gw ** 2) + np.sum(gb ** 2)))
@@ -442,7 +443,7 @@ def linear_train_step(features, tokens, behav, traj_bounds, rewards, W, b, adam_
         n = max(n_valid, 1)
         gw /= n
         gb /= n
-        W, b, m_w, v_w, m_b, v_b, step = _adam(W, b, gw, gb, m_w, v_w, m_b, v_b, step, adam)
+        W, b, m_w, v_w, m_b, v_b, step = adam_update(W, b, gw, gb, m_w, v_w, m_b, v_b, step, adam)
         updates += 1
         loss_sum += -obj
         token_total += n_valid

@@ -13,6 +13,8 @@ import torch  # noqa: F401  (load torch's CUDA runtime before the library)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libareal_b200.so")
+# tuning builds (tools/variants.py) can be selected explicitly; default: the in-tree build
+LIB_PATH = os.environ.get("AREAL_B200_LIB", LIB_PATH)
 
 ABI_VERSION = 1
 N_STATS = 8
@@ -53,6 +55,22 @@ class AdvParams(ctypes.Structure):
                 ("norm", c_i32)]
 
 
+class AdamTensor(ctypes.Structure):
+    """areal_adam_tensor_t"""
+    _fields_ = [("param", c_vp), ("grad", c_vp), ("exp_avg", c_vp), ("exp_avg_sq", c_vp),
+                ("numel", c_i64)]
+
+
+class AdamParams(ctypes.Structure):
+    """areal_adam_params_t"""
+    _fields_ = [("lr", c_f64), ("beta1", c_f64), ("beta2", c_f64), ("eps", c_f64),
+                ("weight_decay", c_f64), ("clip_norm", c_f64), ("one_minus_beta1", c_f64),
+                ("one_minus_beta2", c_f64), ("bias_correction1", c_f64),
+                ("bias_correction2", c_f64), ("grad_scale", c_f64), ("exact_norm", c_i32)]
+
+
+ADAM_MAX_TENSORS = 32
+
 _SIGS = {
     "areal_abi_version": ([], c_i32),
     "areal_status_string": ([ctypes.c_int], ctypes.c_char_p),
@@ -69,6 +87,8 @@ _SIGS = {
                                  c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp],
                                 ctypes.c_int),
     "areal_fill_gather": ([c_vp, c_vp, c_vp, c_i32, c_i64, c_vp, c_vp, c_vp], ctypes.c_int),
+    "areal_adam_step": ([ctypes.POINTER(AdamTensor), c_i32, ctypes.c_int, ctypes.c_int,
+                         ctypes.POINTER(AdamParams), c_vp, c_vp, c_sz, c_vp], ctypes.c_int),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGS)

@@ -12,6 +12,7 @@
 // Extensions (north star): GAE reverse scan per sequence (one warp per
 // trajectory, segmented affine warp scan) and GRPO group normalisation.
 #include "common.cuh"
+#include "pairwise.cuh"
 
 namespace areal {
 
@@ -102,58 +103,14 @@ __device__ __forceinline__ double pw_val(const double* x, int64_t i, int pass, d
   return __dmul_rn(d, d);
 }
 
-__device__ double pw_sum(const double* x, int64_t off, int64_t n, int pass, double mean) {
-  if (n < 8) {
-    double res = 0.0;
-    for (int64_t i = 0; i < n; ++i) res = __dadd_rn(res, pw_val(x, off + i, pass, mean));
-    return res;
-  }
-  if (n <= 128) {
-    double r[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) r[j] = pw_val(x, off + j, pass, mean);
-    int64_t i = 8;
-    for (; i < n - (n % 8); i += 8) {
-#pragma unroll
-      for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], pw_val(x, off + i + j, pass, mean));
-    }
-    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-    for (; i < n; ++i) res = __dadd_rn(res, pw_val(x, off + i, pass, mean));
-    return res;
-  }
-  int64_t n2 = n / 2;
-  n2 -= n2 % 8;
-  return __dadd_rn(pw_sum(x, off, n2, pass, mean), pw_sum(x, off + n2, n - n2, pass, mean));
-}
+struct PwVal {
+  const double* x;
+  int pass;
+  double mean;
+  __device__ double operator()(int64_t i) const { return pw_val(x, i, pass, mean); }
+};
 
-// Depth at which every node of the pairwise tree still splits (size > 128).
-__host__ __device__ inline int pw_depth(int64_t n) {
-  int d = 0;
-  while (d < kMaxTreeDepth && n > 128) {
-    int64_t n2 = n / 2;
-    n2 -= n2 % 8;
-    n = n2;  // leftmost path is the smallest node at each depth
-    ++d;
-  }
-  return d;
-}
-
-__device__ __forceinline__ void pw_node(int64_t n, int depth, int64_t i, int64_t& off,
-                                        int64_t& len) {
-  off = 0;
-  len = n;
-  for (int l = 0; l < depth; ++l) {
-    int64_t n2 = len / 2;
-    n2 -= n2 % 8;
-    if ((i >> (depth - 1 - l)) & 1) {
-      off += n2;
-      len -= n2;
-    } else {
-      len = n2;
-    }
-  }
-}
+__host__ __device__ inline int pw_depth(int64_t n) { return pw_depth(n, kMaxTreeDepth); }
 
 __global__ void pw_leaves_kernel(const double* x, int64_t n, int depth, int pass,
                                  const double* mean_ptr, double* out) {
@@ -162,7 +119,7 @@ __global__ void pw_leaves_kernel(const double* x, int64_t n, int depth, int pass
   int64_t off, len;
   pw_node(n, depth, i, off, len);
   const double mean = pass ? *mean_ptr : 0.0;
-  out[i] = pw_sum(x, off, len, pass, mean);
+  out[i] = pw_sum_f(PwVal{x, pass, mean}, off, len);
 }
 
 // Combine the 2^depth subtree sums in tree order; pass 0 -> mean, pass 1 -> std.

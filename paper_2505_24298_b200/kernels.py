@@ -255,3 +255,58 @@ def fill_gather(traj_bounds, plan: DevicePlan, n_packed_tokens: int, with_seq_id
                                 n_items, int(n_packed_tokens), _ptr(gather), _ptr(seq_id),
                                 _stream()), "areal_fill_gather")
     return gather, seq_id
+
+
+# ---------------------------------------------------------------- K6
+def adam_step(params, grads, exp_avgs, exp_avg_sqs, *, step: int, lr: float, beta1: float,
+              beta2: float, eps: float, weight_decay: float, clip_norm: float,
+              grad_scale: float = 1.0, exact_norm: bool | None = None, norm_out=None):
+    """Fused global-norm clip + Adam over a list of tensors (K6), in place.
+
+    Mirrors policy.apply_update (policy.py:225-258) applied to ``grad * grad_scale``
+    (trainer.py:329-330 passes grad_scale = -1/n).  ``step`` is the optimizer step
+    AFTER this update (the reference's ``opt.step += 1``).  Returns a device float64
+    tensor [global_norm, n_nonfinite]; when n_nonfinite > 0 nothing was updated and
+    the caller raises NonFiniteGradientError.  ``exact_norm`` (default: fp64 params)
+    replays numpy's pairwise sums so the update is bit-identical to the reference.
+    """
+    lib = _lib.load()
+    n = len(params)
+    if not (n == len(grads) == len(exp_avgs) == len(exp_avg_sqs)):
+        raise ValueError("params, grads, exp_avgs, exp_avg_sqs must have the same length")
+    if n > _lib.ADAM_MAX_TENSORS:
+        raise ValueError(f"at most {_lib.ADAM_MAX_TENSORS} tensors per adam_step call")
+    if n == 0:
+        raise ValueError("adam_step needs at least one tensor")
+    dev = params[0].device
+    pdt = params[0].dtype
+    gdt = grads[0].dtype
+    if pdt not in (torch.float64, torch.float32):
+        raise TypeError(f"params must be float64 or float32, got {pdt}")
+    if (pdt == torch.float64) != (gdt == torch.float64) or gdt not in _lib.DTYPE_CODES:
+        raise TypeError(f"grads of dtype {gdt} cannot update {pdt} params "
+                        "(float64 with float64; float32/bfloat16/float16 with float32)")
+    arr = (_lib.AdamTensor * n)()
+    for k in range(n):
+        p, g, m, v = params[k], grads[k], exp_avgs[k], exp_avg_sqs[k]
+        _need(p, f"params[{k}]", pdt, dev)
+        _need(g, f"grads[{k}]", gdt, dev)
+        _need(m, f"exp_avgs[{k}]", pdt, dev)
+        _need(v, f"exp_avg_sqs[{k}]", pdt, dev)
+        if not (p.numel() == g.numel() == m.numel() == v.numel()):
+            raise ValueError(f"tensor {k}: param/grad/moment sizes differ")
+        arr[k] = _lib.AdamTensor(p.data_ptr(), g.data_ptr(), m.data_ptr(), v.data_ptr(), p.numel())
+    if exact_norm is None:
+        exact_norm = pdt == torch.float64 and gdt == torch.float64
+    # scalars exactly as the reference computes them in Python (policy.py:245-250)
+    prm = _lib.AdamParams(float(lr), float(beta1), float(beta2), float(eps), float(weight_decay),
+                          float(clip_norm), 1 - beta1, 1 - beta2, 1 - beta1 ** step,
+                          1 - beta2 ** step, float(grad_scale), int(bool(exact_norm)))
+    if norm_out is None:
+        norm_out = torch.empty(2, dtype=torch.float64, device=dev)
+    _need(norm_out, "norm_out", torch.float64, dev, 2)
+    ws = workspace(dev)
+    check(lib.areal_adam_step(arr, n, _lib.DTYPE_CODES[pdt], _lib.DTYPE_CODES[gdt],
+                              ctypes.byref(prm), _ptr(norm_out), _ptr(ws), ws.numel(), _stream()),
+          "areal_adam_step")
+    return norm_out

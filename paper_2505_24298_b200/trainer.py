@@ -417,7 +417,8 @@ def plan_step(bounds_host: np.ndarray, bounds_dev: torch.Tensor, minibatches: in
 
 
 class _DeviceAdam:
-    """policy.apply_update (policy.py:225-258) as float64 device ops, same op order."""
+    """policy.apply_update (policy.py:225-258) after grad.scale_(-1/n) (trainer.py:330),
+    as one fused K6 launch sequence: numpy-exact global norm, clip, Adam, in place."""
 
     def __init__(self, opt, dev):
         self.opt = opt
@@ -426,26 +427,19 @@ class _DeviceAdam:
         self.m_b = _d(opt.m_bias, torch.float64, dev)
         self.v_b = _d(opt.v_bias, torch.float64, dev)
 
-    def step(self, W, b, gw, gb, cfg):
-        if not (bool(torch.isfinite(gw).all()) and bool(torch.isfinite(gb).all())):
+    def step(self, W, b, gw, gb, cfg, grad_scale=1.0):
+        """W, b are updated in place; gw, gb are the raw (unscaled) gradient sums."""
+        norm = K.adam_step([W, b], [gw, gb], [self.m_w, self.m_b], [self.v_w, self.v_b],
+                           step=self.opt.step + 1, lr=cfg.lr, beta1=cfg.beta1, beta2=cfg.beta2,
+                           eps=cfg.eps, weight_decay=cfg.weight_decay, clip_norm=cfg.clip_norm,
+                           grad_scale=grad_scale, exact_norm=True)
+        bad = int(norm[1].item())
+        if bad:
             raise NonFiniteGradientError(
                 f"non-finite gradient at optimizer step {self.opt.step + 1}: "
-                f"|w|_nan={int(torch.isnan(gw).sum())}, |b|_nan={int(torch.isnan(gb).sum())}")
-        norm = math.sqrt(float((gw ** 2).sum() + (gb ** 2).sum()))
-        if cfg.clip_norm > 0 and norm > cfg.clip_norm:
-            f = cfg.clip_norm / norm
-            gw, gb = gw * f, gb * f
+                f"|w|_nan={int(torch.isnan(gw * grad_scale).sum())}, "
+                f"|b|_nan={int(torch.isnan(gb * grad_scale).sum())}")
         self.opt.step += 1
-        b1, b2 = cfg.beta1, cfg.beta2
-        self.m_w = b1 * self.m_w + (1 - b1) * gw
-        self.v_w = b2 * self.v_w + (1 - b2) * gw ** 2
-        self.m_b = b1 * self.m_b + (1 - b1) * gb
-        self.v_b = b2 * self.v_b + (1 - b2) * gb ** 2
-        c1 = 1 - b1 ** self.opt.step
-        c2 = 1 - b2 ** self.opt.step
-        lr, wd = cfg.lr, cfg.weight_decay
-        W = W - lr * ((self.m_w / c1) / (torch.sqrt(self.v_w / c2) + cfg.eps) + wd * W)
-        b = b - lr * ((self.m_b / c1) / (torch.sqrt(self.v_b / c2) + cfg.eps) + wd * b)
         return W, b
 
     def write_back(self):
@@ -513,7 +507,9 @@ def train_step(batch: TrainBatch, params, opt, config: TrainerConfig = TrainerCo
         s = stats.cpu().numpy()
         n_valid = int(s[1])
         n = max(n_valid, 1)
-        W, b = dadam.step(W, b, gw / n, gb / n, adam_cfg)                # 329-331
+        # dl = -(d obj/d logits), so gw = -grad_w_sum and the reference's scale -1/n
+        # becomes +1/n (sign flips are exact)
+        W, b = dadam.step(W, b, gw, gb, adam_cfg, grad_scale=1.0 / n)    # 329-331
         updates += 1
         loss_sum += -float(s[0])
         clip_sum += float(s[2])

@@ -18,6 +18,9 @@ advantages.npz  `compute_advantages` (trainer.py:114-125) on random rewards /
                 quirk (np.std of a constant that is not exactly representable).
 allocator.npz   `allocate_microbatches` (trainer.py:235-270) on the reference's
                 property-test distributions, hand cases and large Pareto cases.
+adam.npz        `grad.scale_(-1/n)` + `apply_update` (trainer.py:329-331,
+                policy.py:215-258) over 3 consecutive steps: clipped and
+                unclipped gradients, shapes from 1x1 to 64x300.
 trainstep.npz   `train_step` / `decoupled_ppo_loss` / `naive_ppo_loss` on real
                 rollout batches from the reference's RolloutWorker
                 (test_trainer.py:14-26 recipe).
@@ -277,12 +280,51 @@ def make_trainstep(rng):
     np.savez_compressed(os.path.join(OUT, "trainstep.npz"), **flat)
 
 
+# ---------------------------------------------------------------- adam
+def make_adam():
+    rng = np.random.default_rng(7)
+    cases = []
+    specs = [  # (V, F, grad magnitude per step, lr, clip_norm, weight_decay)
+        (1, 1, (0.3, 50.0, 1e-3), 2e-2, 1.0, 0.05),
+        (16, 12, (1e-2, 1e-2, 3.0), 2e-2, 1.0, 0.05),
+        (37, 185, (5.0, 1e-4, 0.2), 2e-2, 1.0, 0.05),
+        (64, 300, (1e-3, 40.0, 1.0), 1e-3, 1.0, 0.05),
+        (64, 33, (2.0, 2.0, 2.0), 2e-2, 0.0, 0.0),  # clipping disabled
+    ]
+    for V, F, mags, lr, clip, wd in specs:
+        cfg = P.AdamConfig(lr=lr, clip_norm=clip, weight_decay=wd)
+        params = P.VersionedParams(0, rng.normal(0, 0.5, size=(V, F)), rng.normal(0, 0.5, size=V))
+        opt = P.AdamState.zeros_like(params)
+        case = dict(W0=np.array(params.weights), b0=np.array(params.bias), lr=np.array(lr),
+                    clip=np.array(clip), wd=np.array(wd), steps=np.array(len(mags)))
+        for k, mag in enumerate(mags):
+            gw = rng.normal(0, mag, size=(V, F))
+            gb = rng.normal(0, mag, size=V)
+            n = int(rng.integers(1, 5000))
+            grad = P.ParamGrad(gw.copy(), gb.copy())
+            grad.scale_(-1.0 / n)                                    # trainer.py:330
+            norm = grad.global_norm()
+            params = P.apply_update(params, grad, opt, cfg)          # trainer.py:331
+            case.update({f"gw{k}": gw, f"gb{k}": gb, f"n{k}": np.array(n),
+                         f"norm{k}": np.array(norm), f"step{k}": np.array(opt.step)})
+        case.update(W=np.array(params.weights), b=np.array(params.bias), mw=opt.m_weights.copy(),
+                    vw=opt.v_weights.copy(), mb=opt.m_bias.copy(), vb=opt.v_bias.copy())
+        cases.append(case)
+    flat = {f"c{i}_{k}": v for i, c in enumerate(cases) for k, v in c.items()}
+    flat["n_cases"] = np.array(len(cases))
+    np.savez_compressed(os.path.join(OUT, "adam.npz"), **flat)
+
+
 if __name__ == "__main__":
+    only = set(sys.argv[1:])
     rng = np.random.default_rng(20250530)
-    make_surrogate(rng)
-    make_advantages(rng)
-    make_allocator(rng)
-    make_trainstep(rng)
+    if not only:
+        make_surrogate(rng)
+        make_advantages(rng)
+        make_allocator(rng)
+        make_trainstep(rng)
+    if not only or "adam" in only:
+        make_adam()
     for f in sorted(os.listdir(OUT)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(OUT, f)))

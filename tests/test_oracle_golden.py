@@ -258,3 +258,22 @@ def test_stale_mask_disabled_is_reference():
     stale = (8 - ver) > 4
     assert c["stats"][5] == stale.sum()
     assert np.all(c["dlogits"][stale] == 0)
+
+
+def test_adam_oracle_bit_exact_vs_reference_golden():
+    """oracle._adam (policy.py:225-258 restated) reproduces the reference's
+    apply_update after grad.scale_(-1/n) bit for bit over 3 chained steps."""
+    for c in load_cases("adam.npz"):
+        cfg = O.AdamCfg(lr=float(c["lr"]), clip_norm=float(c["clip"]), weight_decay=float(c["wd"]))
+        W, b = c["W0"], c["b0"]
+        m_w, v_w = np.zeros_like(W), np.zeros_like(W)
+        m_b, v_b = np.zeros_like(b), np.zeros_like(b)
+        step = 0
+        for k in range(int(c["steps"])):
+            s = -1.0 / int(c[f"n{k}"])
+            gw, gb = c[f"gw{k}"] * s, c[f"gb{k}"] * s
+            assert math.sqrt(float(np.sum(gw ** 2) + np.sum(gb ** 2))) == float(c[f"norm{k}"])
+            W, b, m_w, v_w, m_b, v_b, step = O.adam_update(W, b, gw, gb, m_w, v_w, m_b, v_b, step, cfg)
+            assert step == int(c[f"step{k}"])
+        for got, key in ((W, "W"), (b, "b"), (m_w, "mw"), (v_w, "vw"), (m_b, "mb"), (v_b, "vb")):
+            assert np.array_equal(got, c[key]), key
