@@ -74,25 +74,28 @@ __device__ __forceinline__ uint32_t tmem_addr(uint32_t base, int warp, int t) {
 }
 
 // This thread's share of a chunk as 16 raw 32-bit words (4 x 16-byte vectors).
+// FULL: the chunk is a whole 32 KB (no per-vector bounds checks).
+template <bool FULL = false>
 __device__ __forceinline__ void lds_raw(const uint4* q, int warp, int lane, int nvec,
                                         uint32_t (&w)[16]) {
 #pragma unroll
   for (int j = 0; j < kVecPerThread; ++j) {
     const int vi = vec_index(warp, lane, j);
     uint4 v = make_uint4(0, 0, 0, 0);
-    if (nvec == kChunkBytes / 16 || vi < nvec) v = q[vi];
+    if (FULL || vi < nvec) v = q[vi];
     w[4 * j + 0] = v.x;
     w[4 * j + 1] = v.y;
     w[4 * j + 2] = v.z;
     w[4 * j + 3] = v.w;
   }
 }
+template <bool FULL = false>
 __device__ __forceinline__ void sts_raw(uint4* q, int warp, int lane, int nvec,
                                         const uint32_t (&w)[16]) {
 #pragma unroll
   for (int j = 0; j < kVecPerThread; ++j) {
     const int vi = vec_index(warp, lane, j);
-    if (nvec == kChunkBytes / 16 || vi < nvec)
+    if (FULL || vi < nvec)
       q[vi] = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
   }
 }
@@ -106,7 +109,7 @@ template <> struct EFmt<float> { using V = Vec<float>; };
 
 // Pass-1 fold of one chunk held as raw words: warp-uniform running max, e computed
 // once, the e words returned in place of the logits and the shift c returned.
-template <typename T, bool ENT>
+template <typename T, bool ENT, bool FULL>
 __device__ __forceinline__ float fold_to_e(RowStat<float>& rs, uint32_t (&w)[16], int warp, int lane,
                                            int nvec) {
   constexpr int E = Vec<T>::N;
@@ -116,7 +119,7 @@ __device__ __forceinline__ float fold_to_e(RowStat<float>& rs, uint32_t (&w)[16]
   for (int j = 0; j < kVecPerThread; ++j) {
     float g[E];
     Vec<T>::unpack(make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]), g);
-    const bool ok = nvec == kChunkBytes / 16 || vec_index(warp, lane, j) < nvec;
+    const bool ok = FULL || vec_index(warp, lane, j) < nvec;
 #pragma unroll
     for (int e = 0; e < E; ++e) f[j * E + e] = ok ? g[e] : Lim<float>::ninf();
   }
@@ -157,6 +160,19 @@ __device__ __forceinline__ float fold_to_e(RowStat<float>& rs, uint32_t (&w)[16]
   if (ENT) rs.sx = rs.sx * r + (x2.x + x2.y);
   rs.m = mn;
   return c;
+}
+
+// Pass-1 step on one ring chunk: load this thread's words, fold them to e (returns
+// the shift c); full 32 KB chunks take the branch-free path.
+template <typename T, bool ENT>
+__device__ __forceinline__ float chunk_to_e(RowStat<float>& rs, const uint4* q, uint32_t (&wv)[16],
+                                            int warp, int lane, int nvec) {
+  if (nvec == kChunkBytes / 16) {
+    lds_raw<true>(q, warp, lane, nvec, wv);
+    return fold_to_e<T, ENT, true>(rs, wv, warp, lane, nvec);
+  }
+  lds_raw<false>(q, warp, lane, nvec, wv);
+  return fold_to_e<T, ENT, false>(rs, wv, warp, lane, nvec);
 }
 
 template <typename T, bool ENT>
@@ -307,8 +323,7 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
         const int nvec = (c < nfull ? kChunkBytes : last_bytes) / 16;
         uint4* q = reinterpret_cast<uint4*>(ring + (size_t)cc.slot * kChunkBytes);
         uint32_t wv[16];
-        lds_raw(q, warp, lane, nvec, wv);
-        const float cshift = fold_to_e<T, ENT>(rs, wv, warp, lane, nvec);
+        const float cshift = chunk_to_e<T, ENT>(rs, q, wv, warp, lane, nvec);
         if (lane == 0) cw[c * kConsumerWarps + warp] = cshift;
         if (c < ntm) {
           tmem_st16(tmem_addr(tbase, warp, c), wv);
@@ -340,8 +355,7 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
         const int nvec = (c < nfull ? kChunkBytes : last_bytes) / 16;
         uint4* q = reinterpret_cast<uint4*>(ring + (size_t)lc.slot * kChunkBytes);
         uint32_t wv[16];
-        lds_raw(q, warp, lane, nvec, wv);
-        const float cshift = fold_to_e<T, ENT>(nxt, wv, warp, lane, nvec);
+        const float cshift = chunk_to_e<T, ENT>(nxt, q, wv, warp, lane, nvec);
         if (lane == 0) cwn[c * kConsumerWarps + warp] = cshift;
         sts_raw(q, warp, lane, nvec, wv);
         lc.next(nslots);
@@ -355,56 +369,54 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
       const float lse_s = (float)b.lse;
       const T dtok = from_bits<T>(b.dtok);
       char* drow = a.dlogits + row * a.ld_out_bytes;
-      // ---- pass 2: dlogits = e * g 2^(c - lse) (one-hot element patched), 16-byte stores
+      // ---- pass 2: dlogits = e * g 2^(c - lse), 16-byte stores.  Full chunks are
+      // branch-free; the one-hot element is patched afterwards by the thread that
+      // stored its vector (same-thread program order => the patch lands last).
+      // g == 0 rows still multiply (0 * e): NaN/inf logits give NaN, like the
+      // reference's coef * (onehot - softmax).
       Cursor c2 = cur;
       for (int c = 0; c < nchunks; ++c) {
-        const int cbytes = c < nfull ? kChunkBytes : last_bytes;
-        const int nvec = cbytes / 16;
+        const bool full = c < nfull;
+        const int nvec = (full ? kChunkBytes : last_bytes) / 16;
         uint32_t wv[16];
-        if (g != 0.f) {
-          if (c < ntm) {
-            tmem_ld16(tmem_addr(tbase, warp, c), wv);
-            tmem_wait_ld();
-          } else {  // resident tail chunk (its full barrier completed in pass 1)
-            lds_raw(reinterpret_cast<const uint4*>(ring + (size_t)c2.slot * kChunkBytes), warp,
-                    lane, nvec, wv);
-          }
-        }
-        if (c >= ntm) {
+        if (c < ntm) {
+          tmem_ld16(tmem_addr(tbase, warp, c), wv);
+          tmem_wait_ld();
+        } else {  // resident tail chunk (its full barrier completed in pass 1)
+          const uint4* q = reinterpret_cast<const uint4*>(ring + (size_t)c2.slot * kChunkBytes);
+          if (full) lds_raw<true>(q, warp, lane, nvec, wv);
+          else lds_raw<false>(q, warp, lane, nvec, wv);
           __syncwarp();
           if (lane == 0) mbar_arrive(&empty[c2.slot]);
         }
         const float F = g * fast_exp2(cw[c * kConsumerWarps + warp] - lse_s);
         const float2 F2 = make_float2(F, F);
-        const int64_t toff = b.tok - (int64_t)c * (kChunkBytes / (int)sizeof(T));
         uint4* dst = reinterpret_cast<uint4*>(drow + (size_t)c * kChunkBytes);
 #pragma unroll
         for (int j = 0; j < kVecPerThread; ++j) {
           const int vi = vec_index(warp, lane, j);
-          if (nvec == kChunkBytes / 16 || vi < nvec) {
+          if (full || vi < nvec) {
             float f[E];
-            if (g == 0.f) {
+            EFmt<T>::V::unpack(make_uint4(wv[4 * j], wv[4 * j + 1], wv[4 * j + 2], wv[4 * j + 3]), f);
 #pragma unroll
-              for (int e = 0; e < E; ++e) f[e] = 0.f;
-            } else {
-              EFmt<T>::V::unpack(make_uint4(wv[4 * j], wv[4 * j + 1], wv[4 * j + 2], wv[4 * j + 3]), f);
-#pragma unroll
-              for (int e = 0; e < E; e += 2) {
-                const float2 d = fmul2(make_float2(f[e], f[e + 1]), F2);
-                f[e] = d.x;
-                f[e + 1] = d.y;
-              }
-              const int64_t eoff = toff - (int64_t)vi * E;
-              if (eoff >= 0 && eoff < E) {  // the one-hot element (exact: a T value)
-#pragma unroll
-                for (int e = 0; e < E; ++e)
-                  if (e == eoff) f[e] = Traits<T>::to_acc(dtok);
-              }
+            for (int e = 0; e < E; e += 2) {
+              const float2 d = fmul2(make_float2(f[e], f[e + 1]), F2);
+              f[e] = d.x;
+              f[e + 1] = d.y;
             }
             dst[vi] = Vec<T>::pack(f);
           }
         }
         c2.next(nslots);
+      }
+      {  // the one-hot element: owner of vector vt of chunk ct
+        const int64_t per_chunk = kChunkBytes / (int)sizeof(T);
+        if (b.tok >= 0 && b.tok < a.vocab) {
+          const int ct = (int)(b.tok / per_chunk);
+          const int vt = (int)((b.tok - (int64_t)ct * per_chunk) / E);
+          if (warp == vt / (kWarpBytes / 16) && lane == (vt & 31))
+            reinterpret_cast<T*>(drow)[b.tok] = dtok;
+        }
       }
       cur = after;
     }
