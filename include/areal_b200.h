@@ -176,6 +176,24 @@ int areal_fill_gather(const int64_t* traj_bounds, const int32_t* packed_traj,
                       const int64_t* seq_cu, int32_t n_items, int64_t n_packed_tokens,
                       int32_t* gather, int32_t* seq_id, void* stream);
 
+/* ---- K7: fused LM-head GEMM + log-softmax-gather (+ entropy), tcgen05 ----------
+ * Replaces recompute_prox_logprobs (trainer.py:128-137) including the model's output
+ * layer: logits = features @ W.T + b (policy.py:133-142, called from
+ * batch_token_log_probs, policy.py:159-163), then log_softmax (policy.py:145-147)
+ * gathered at the token.  hidden [n_rows, dim] and weight [vocab, dim] are 16-bit
+ * (dtype BF16 or F16, row strides ld_* in elements, multiples of 8, 16-byte aligned
+ * bases); bias [vocab] fp32 or NULL; dim % 64 == 0.  Row r's global token index is
+ * row_index[r] (NULL = r): lp_out[idx] = x[tok] - logsumexp(x), entropy_out (may be
+ * NULL) = -sum p log p, x = hidden[r] . weight^T + bias accumulated in fp32 on the
+ * tensor cores.  The [n_rows, vocab] logits never reach HBM.  scratch (device) holds
+ * per-(row, 2048-column block) partials: areal_linear_logprob_scratch_bytes(). */
+size_t areal_linear_logprob_scratch_bytes(int64_t n_rows, int64_t vocab);
+int areal_linear_logprob_fwd(const void* hidden, int64_t ld_hidden, const void* weight,
+                             int64_t ld_weight, const float* bias, int dtype, int64_t n_rows,
+                             int64_t vocab, int64_t dim, const int64_t* tokens,
+                             const int32_t* row_index, double* lp_out, double* entropy_out,
+                             void* scratch, size_t scratch_bytes, void* stream);
+
 /* ---- K6: fused global-norm clip + Adam (decoupled weight decay), multi-tensor --
  * Replaces the optimizer step of train_step (trainer.py:329-331): grad.scale_(-1/n)
  * then apply_update (policy.py:225-258) with clip_by_global_norm (policy.py:215-221).

@@ -1,0 +1,416 @@
+// linear_lp.cu — K7: fused LM-head GEMM + log-softmax-gather (+ entropy) on tcgen05.
+//
+// Reference: recompute_prox_logprobs (trainer.py:128-137) -> batch_token_log_probs
+// (policy.py:159-163) -> logits(params, features) = features @ W.T + b
+// (policy.py:133-142) -> log_softmax (policy.py:145-147), gathered at the token.
+// Here features are the model's hidden states H [T, d] (bf16/fp16) and W [V, d] is the
+// LM head; the [T, V] logits are never written to HBM.
+//
+// Structure (persistent, one CTA per SM, warp-specialised, 192 threads):
+//   warp 0      TMA producer: 2-D tensor-map loads of H [128 x 64] and W [256 x 64]
+//               k-slabs (128-byte swizzle) into a 4-stage shared-memory ring
+//   warp 1      MMA issuer: one elected lane issues tcgen05.mma.cta_group::1.kind::f16
+//               (M=128, N=256, K=16) from shared-memory descriptors into a TMEM
+//               accumulator; two accumulators (2 x 256 of the 512 TMEM columns) so
+//               the epilogue of N-tile j overlaps the MMAs of N-tile j+1
+//   warps 2-5   epilogue: tcgen05.ld 32x32b (thread = token row, 32 columns per load),
+//               + bias, online (max, sum 2^x, sum 2^x * x) per row, the token's logit
+//               picked out when its column passes; TMEM slot released by mbarrier
+// A work unit is (128-token tile, 2048-column vocab block); units are ordered
+// vocab-block-major so the CTAs running together share one W block in L2.  Each unit
+// writes a per-(row, block) partial {m, s, sx, x_tok}; a merge kernel folds a row's
+// partials in block order (deterministic) into lp = x_tok - lse and H = lse - sx/s.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace areal {
+namespace k7 {
+
+constexpr int BM = 128;            // tokens per tile (TMEM lanes)
+constexpr int BN = 256;            // vocab columns per MMA / accumulator
+constexpr int BK = 64;             // k-slab: 64 x 2 B = one 128-byte swizzle row
+constexpr int UMMA_K = 16;         // K per tcgen05.mma for 16-bit inputs
+constexpr int STAGES = 4;
+constexpr int NT = 8;              // N-tiles per unit
+constexpr int VB = NT * BN;        // vocab block per unit
+constexpr int A_BYTES = BM * BK * 2;
+constexpr int B_BYTES = BN * BK * 2;
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int THREADS = 192;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024;  // + alignment slack for SW128
+
+struct Args {
+  const float* bias;
+  const int64_t* tokens;
+  const int32_t* row_index;
+  float4* partials;  // [n_rows, n_vb]
+  int64_t n_rows, vocab;
+  int32_t dim, n_mt, n_vb, n_units;
+  uint32_t idesc;
+};
+
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, void* smem_dst, uint64_t* bar,
+                                            int32_t x, int32_t y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::
+          "r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+// K-major, 128-byte-swizzled operand tile: rows of 128 B, 8-row groups 1024 B apart
+// (SBO = 1024 B, LBO unused = 16 B), descriptor version 1 (sm_100), layout SWIZZLE_128B.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t smem_addr) {
+  const uint32_t lo = ((smem_addr >> 4) & 0x3FFFu) | (1u << 16);
+  const uint32_t hi = (1024u >> 4) | (1u << 14) | (2u << 29);
+  return ((uint64_t)hi << 32) | lo;
+}
+
+__device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, "
+      "%30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr)
+      : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+struct Pipe {
+  uint32_t stage = 0, phase = 0;
+  __device__ __forceinline__ void next() {
+    if (++stage == STAGES) {
+      stage = 0;
+      phase ^= 1u;
+    }
+  }
+};
+
+template <bool ENT>
+__global__ void __launch_bounds__(THREADS, 1)
+    linear_lp_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const Args a) {
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2];
+  __shared__ uint32_t s_tbase;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ksteps = a.dim / BK;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 4);  // one arrive per epilogue warp
+    }
+    fence_mbar_init_cluster();
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(&s_tbase))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    tc_fence_before();
+  }
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = s_tbase;
+
+  if (warp == 0) {
+    // ================= TMA producer
+    if (lane == 0) {
+      Pipe p;
+      for (int u = blockIdx.x; u < a.n_units; u += gridDim.x) {
+        const int mt = u % a.n_mt, vb = u / a.n_mt;
+        for (int n = 0; n < NT; ++n) {
+          const int64_t n0 = (int64_t)vb * VB + (int64_t)n * BN;
+          if (n0 >= a.vocab) break;
+          for (int ks = 0; ks < ksteps; ++ks) {
+            mbar_wait(&empty[p.stage], p.phase ^ 1u);
+            unsigned char* st = smem + (size_t)p.stage * STAGE_BYTES;
+            mbar_arrive_expect_tx(&full[p.stage], STAGE_BYTES);
+            tma_load_2d(&tmA, st, &full[p.stage], ks * BK, mt * BM);
+            tma_load_2d(&tmB, st + A_BYTES, &full[p.stage], ks * BK, (int32_t)n0);
+            p.next();
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer
+    if (lane == 0) {
+      Pipe p;
+      uint32_t acc = 0, acc_phase = 0;
+      for (int u = blockIdx.x; u < a.n_units; u += gridDim.x) {
+        const int vb = u / a.n_mt;
+        for (int n = 0; n < NT; ++n) {
+          const int64_t n0 = (int64_t)vb * VB + (int64_t)n * BN;
+          if (n0 >= a.vocab) break;
+          mbar_wait(&tempty[acc], acc_phase ^ 1u);
+          tc_fence_after();
+          const uint32_t d_tmem = tbase + acc * BN;
+          for (int ks = 0; ks < ksteps; ++ks) {
+            mbar_wait(&full[p.stage], p.phase);
+            tc_fence_after();
+            const uint32_t sa = smem_u32(smem + (size_t)p.stage * STAGE_BYTES);
+            const uint64_t adesc = sw128_desc(sa), bdesc = sw128_desc(sa + A_BYTES);
+#pragma unroll
+            for (int kk = 0; kk < BK / UMMA_K; ++kk) {
+              // advance the start address by kk * 32 bytes inside the swizzle row
+              mma_bf16(d_tmem, adesc + (uint64_t)(kk * 2), bdesc + (uint64_t)(kk * 2), a.idesc,
+                       (ks | kk) != 0);
+            }
+            mma_commit(&empty[p.stage]);  // frees the stage once these MMAs have read it
+            p.next();
+          }
+          mma_commit(&tfull[acc]);  // accumulator complete -> epilogue
+          acc ^= 1u;
+          if (acc == 0) acc_phase ^= 1u;
+        }
+      }
+    }
+  } else {
+    // ================= epilogue: one thread per token row
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int r_local = q * 32 + lane;
+    const uint32_t lane_base = tbase + ((uint32_t)(q * 32) << 16);
+    uint32_t acc = 0, acc_phase = 0;
+    constexpr float L2E = 1.4426950408889634f;
+    for (int u = blockIdx.x; u < a.n_units; u += gridDim.x) {
+      const int mt = u % a.n_mt, vb = u / a.n_mt;
+      const int64_t row = (int64_t)mt * BM + r_local;
+      int64_t tok = -1;
+      if (row < a.n_rows) {
+        const int64_t idx = a.row_index ? (int64_t)a.row_index[row] : row;
+        tok = a.tokens[idx];
+      }
+      float m = -INFINITY, s = 0.f, sx = 0.f, xa = 0.f;
+      for (int n = 0; n < NT; ++n) {
+        const int64_t n0 = (int64_t)vb * VB + (int64_t)n * BN;
+        if (n0 >= a.vocab) break;
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+#pragma unroll 1
+        for (int ch = 0; ch < BN / 32; ++ch) {
+          float v[32];
+          tmem_ld32(lane_base + acc * BN + ch * 32, v);
+          const int64_t c0 = n0 + ch * 32;
+          if (a.bias != nullptr) {
+            const float4* b4 = reinterpret_cast<const float4*>(a.bias + c0);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              if (c0 + 4 * i + 3 < a.vocab) {
+                const float4 bb = __ldg(b4 + i);
+                v[4 * i] += bb.x;
+                v[4 * i + 1] += bb.y;
+                v[4 * i + 2] += bb.z;
+                v[4 * i + 3] += bb.w;
+              } else {
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                  if (c0 + 4 * i + e < a.vocab) v[4 * i + e] += __ldg(a.bias + c0 + 4 * i + e);
+              }
+            }
+          }
+          if (c0 + 32 > a.vocab) {  // vocab tail: columns past V are padding
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (c0 + i >= a.vocab) v[i] = -INFINITY;
+          }
+          if (tok >= c0 && tok < c0 + 32) {  // rare: the token's logit
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (c0 + i == tok) xa = v[i];
+          }
+          float lmax = v[0];
+#pragma unroll
+          for (int i = 1; i < 32; ++i) lmax = fmaxf(lmax, v[i]);
+          const float mn = fmaxf(m, lmax);
+          const float c = (mn == -INFINITY) ? 0.f : mn * L2E;
+          const float r = fast_exp2(fmaf(m, L2E, -c));
+          const float2 L2 = make_float2(L2E, L2E), C2 = make_float2(-c, -c);
+          float2 s2 = make_float2(0.f, 0.f), x2 = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            const float2 x = make_float2(v[i], v[i + 1]);
+            const float2 t = ffma2(x, L2, C2);
+            const float2 e = make_float2(fast_exp2(t.x), fast_exp2(t.y));
+            s2 = fadd2(s2, e);
+            if (ENT) {
+              const float2 xc = make_float2(fmaxf(x.x, -3.402823466e38f), fmaxf(x.y, -3.402823466e38f));
+              x2 = ffma2(e, xc, x2);
+            }
+          }
+          s = s * r + (s2.x + s2.y);
+          if (ENT) sx = sx * r + (x2.x + x2.y);
+          m = mn;
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        acc ^= 1u;
+        if (acc == 0) acc_phase ^= 1u;
+      }
+      if (row < a.n_rows) a.partials[row * a.n_vb + vb] = make_float4(m, s, sx, xa);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tbase) : "memory");
+  }
+}
+
+// One warp per row: merge the row's block partials in block order.
+__global__ void linear_lp_merge_kernel(const float4* partials, int n_vb, int64_t n_rows, int64_t vocab,
+                                       const int64_t* tokens, const int32_t* row_index, double* lp,
+                                       double* ent) {
+  const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= n_rows) return;
+  RowStat<float> w;
+  w.init();
+  for (int j = lane; j < n_vb; j += 32) {
+    const float4 p = partials[row * n_vb + j];
+    w.merge(p.x, p.y, p.z);
+  }
+  // fixed-order butterfly: identical on every lane, deterministic
+  w.warp_reduce();
+  if (lane == 0) {
+    const int64_t idx = row_index ? (int64_t)row_index[row] : row;
+    const int64_t tok = tokens[idx];
+    const double lse = (double)w.m + log((double)w.s);
+    double xa = nan("");
+    if (tok >= 0 && tok < vocab) xa = (double)partials[row * n_vb + tok / VB].w;
+    lp[idx] = xa - lse;
+    if (ent) ent[idx] = lse - (double)w.sx / (double)w.s;
+  }
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return nullptr;
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 2-D K-major tile map: rows x dim (16-bit elements, row stride ld elements), box
+// [box_rows x 64], 128-byte swizzle, out-of-bounds rows zero-filled.
+static bool make_map(CUtensorMap* map, const void* base, CUtensorMapDataType dt, int64_t rows,
+                     int64_t dim, int64_t ld, int box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)dim, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return fn(map, dt, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace k7
+}  // namespace areal
+
+using namespace areal;
+
+extern "C" size_t areal_linear_logprob_scratch_bytes(int64_t n_rows, int64_t vocab) {
+  const int64_t n_vb = (vocab + k7::VB - 1) / k7::VB;
+  return (size_t)(n_rows > 0 ? n_rows : 0) * (size_t)n_vb * sizeof(float4);
+}
+
+extern "C" int areal_linear_logprob_fwd(const void* hidden, int64_t ld_hidden, const void* weight,
+                                        int64_t ld_weight, const float* bias, int dtype, int64_t n_rows,
+                                        int64_t vocab, int64_t dim, const int64_t* tokens,
+                                        const int32_t* row_index, double* lp_out, double* entropy_out,
+                                        void* scratch, size_t scratch_bytes, void* stream_) {
+  using namespace areal::k7;
+  if (n_rows < 0 || vocab < 1 || dim < 1) return AREAL_ERR_BAD_SHAPE;
+  if (n_rows == 0) return AREAL_OK;
+  if (!hidden || !weight || !tokens || !lp_out) return AREAL_ERR_INVALID_ARGUMENT;
+  if (dtype != AREAL_BF16 && dtype != AREAL_F16) return AREAL_ERR_BAD_DTYPE;
+  if (dim % BK != 0 || dim > 65536) return AREAL_ERR_UNSUPPORTED;
+  if (ld_hidden < dim || ld_weight < dim || ld_hidden % 8 || ld_weight % 8 ||
+      reinterpret_cast<uintptr_t>(hidden) % 16 || reinterpret_cast<uintptr_t>(weight) % 16 ||
+      (bias && reinterpret_cast<uintptr_t>(bias) % 16))
+    return AREAL_ERR_MISALIGNED;
+  if (n_rows > ((int64_t)1 << 31) - BM || vocab > ((int64_t)1 << 31) - VB) return AREAL_ERR_BAD_SHAPE;
+  if (!scratch || scratch_bytes < areal_linear_logprob_scratch_bytes(n_rows, vocab)) return AREAL_ERR_WORKSPACE;
+  const CUtensorMapDataType dt = dtype == AREAL_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  CUtensorMap tmA, tmB;
+  if (!make_map(&tmA, hidden, dt, n_rows, dim, ld_hidden, BM) ||
+      !make_map(&tmB, weight, dt, vocab, dim, ld_weight, BN))
+    return AREAL_ERR_CUDA;
+  Args a;
+  a.bias = bias;
+  a.tokens = tokens;
+  a.row_index = row_index;
+  a.partials = static_cast<float4*>(scratch);
+  a.n_rows = n_rows;
+  a.vocab = vocab;
+  a.dim = (int32_t)dim;
+  a.n_mt = (int32_t)((n_rows + BM - 1) / BM);
+  a.n_vb = (int32_t)((vocab + VB - 1) / VB);
+  a.n_units = a.n_mt * a.n_vb;
+  // kind::f16 instruction descriptor: D fp32, A/B bf16 (1) or fp16 (0), both K-major,
+  // N >> 3 at bit 17, M >> 4 at bit 24 (cute::UMMA::InstrDescriptor)
+  const uint32_t ab = dtype == AREAL_BF16 ? 1u : 0u;
+  a.idesc = (1u << 4) | (ab << 7) | (ab << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = std::min(sms, a.n_units);
+  auto kern = entropy_out ? linear_lp_kernel<true> : linear_lp_kernel<false>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  kern<<<grid, THREADS, SMEM_BYTES, stream>>>(tmA, tmB, a);
+  AREAL_CUDA_CHECK_LAUNCH();
+  const int64_t threads = n_rows * 32;
+  linear_lp_merge_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, stream>>>(
+      a.partials, a.n_vb, n_rows, vocab, tokens, row_index, lp_out, entropy_out);
+  AREAL_CUDA_CHECK_LAUNCH();
+  return AREAL_OK;
+}

@@ -310,3 +310,58 @@ def adam_step(params, grads, exp_avgs, exp_avg_sqs, *, step: int, lr: float, bet
                               ctypes.byref(prm), _ptr(norm_out), _ptr(ws), ws.numel(), _stream()),
           "areal_adam_step")
     return norm_out
+
+
+# ---------------------------------------------------------------- K7
+_SCRATCH: dict = {}
+
+
+def _scratch(dev, nbytes):
+    key = (dev.index, torch.cuda.current_stream(dev).cuda_stream)
+    buf = _SCRATCH.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=dev)
+        _SCRATCH[key] = buf
+    return buf
+
+
+def linear_logprob_fwd(hidden: torch.Tensor, weight: torch.Tensor, tokens: torch.Tensor,
+                       bias: torch.Tensor | None = None, row_index: torch.Tensor | None = None,
+                       lp_out=None, entropy_out=None, with_entropy: bool = False):
+    """Fused LM head + log-softmax-gather (K7, tcgen05): lp[idx] = log_softmax(h W^T + b)[tok].
+
+    ``hidden`` [n, d] and ``weight`` [V, d] are bf16/fp16 (row-contiguous, d % 64 == 0),
+    ``bias`` fp32 [V] or None.  Mirrors recompute_prox_logprobs / batch_token_log_probs
+    (trainer.py:128-137, policy.py:133-163) with the output layer fused in: the [n, V]
+    logits are never materialised.  Returns (lp, entropy-or-None), float64, indexed like K1.
+    """
+    lib = _lib.load()
+    if hidden.dim() != 2 or weight.dim() != 2 or hidden.shape[1] != weight.shape[1]:
+        raise ValueError("hidden [n, d] and weight [V, d] must share d")
+    if hidden.dtype not in (torch.bfloat16, torch.float16) or weight.dtype != hidden.dtype:
+        raise TypeError("hidden and weight must both be bfloat16 or float16")
+    if hidden.stride(1) != 1 or weight.stride(1) != 1:
+        raise ValueError("hidden / weight rows must be contiguous")
+    dev = hidden.device
+    n, d = hidden.shape
+    V = weight.shape[0]
+    if bias is not None:
+        _need(bias, "bias", torch.float32, dev, V)
+    _need(tokens, "tokens", torch.int64, dev)
+    if row_index is not None:
+        _need(row_index, "row_index", torch.int32, dev, n)
+    n_idx = tokens.numel() if row_index is not None else n
+    if lp_out is None:
+        lp_out = torch.empty(n_idx, dtype=torch.float64, device=dev)
+    if with_entropy and entropy_out is None:
+        entropy_out = torch.empty(n_idx, dtype=torch.float64, device=dev)
+    nbytes = int(lib.areal_linear_logprob_scratch_bytes(n, V))
+    scratch = _scratch(dev, nbytes)
+    ld_h = hidden.stride(0) if n > 1 else d
+    ld_w = weight.stride(0) if V > 1 else d
+    check(lib.areal_linear_logprob_fwd(_ptr(hidden), ld_h, _ptr(weight), ld_w, _ptr(bias),
+                                       _lib.DTYPE_CODES[hidden.dtype], n, V, d, _ptr(tokens),
+                                       _ptr(row_index), _ptr(lp_out), _ptr(entropy_out),
+                                       _ptr(scratch), scratch.numel(), _stream()),
+          "areal_linear_logprob_fwd")
+    return lp_out, entropy_out

@@ -1,0 +1,89 @@
+"""K7 fused LM-head + log-softmax-gather (areal_linear_logprob_fwd, tcgen05) vs the
+float64 oracle: recompute_prox_logprobs with the model's output layer
+(logits = features @ W.T + b, policy.py:133-163; trainer.py:128-137), computed from
+the same 16-bit values in float64.  The fused kernel accumulates in fp32 on the
+tensor cores and never rounds logits to 16 bits, so the tolerance is fp32-level."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_2505_24298_b200 import kernels as K
+
+DEV = "cuda"
+ATOL = 2e-4
+
+
+def _case(n, V, d, dtype=torch.bfloat16, bias=True, seed=0, scale=1.0):
+    g = torch.Generator(device=DEV).manual_seed(seed)
+    h = (torch.randn(n, d, device=DEV, generator=g) * scale).to(dtype)
+    w = (torch.randn(V, d, device=DEV, generator=g) / d ** 0.5 * 4).to(dtype)
+    b = torch.randn(V, device=DEV, generator=g) if bias else None
+    tok = torch.randint(0, V, (n,), device=DEV, generator=g)
+    return h, w, b, tok
+
+
+def _ref(h, w, b, tok, entropy=True):
+    x = h.double() @ w.double().t()
+    if b is not None:
+        x = x + b.double()
+    lse = torch.logsumexp(x, dim=1)
+    lp = x.gather(1, tok[:, None])[:, 0] - lse
+    ent = None
+    if entropy:
+        p = torch.softmax(x, dim=1)
+        ent = -(p * torch.log_softmax(x, dim=1)).sum(1)
+    return lp, ent
+
+
+@pytest.mark.parametrize("n,V,d", [(1, 1000, 64), (100, 4096, 128), (300, 32000, 256),
+                                   (129, 2049, 64), (257, 151936, 1536), (64, 152064, 512)])
+def test_linear_logprob_matches_float64(n, V, d):
+    h, w, b, tok = _case(n, V, d)
+    lp, ent = K.linear_logprob_fwd(h, w, tok, bias=b, with_entropy=True)
+    rlp, rent = _ref(h, w, b, tok)
+    torch.testing.assert_close(lp, rlp, rtol=0, atol=ATOL)
+    torch.testing.assert_close(ent, rent, rtol=1e-5, atol=ATOL)
+
+
+def test_linear_logprob_numpy_oracle_small():
+    # the CPU oracle (linear_logits + token_logprobs) on the same bf16 values
+    h, w, b, tok = _case(37, 517, 64, seed=3)
+    lp, ent = K.linear_logprob_fwd(h, w, tok, bias=b, with_entropy=True)
+    x = O.linear_logits(h.double().cpu().numpy(), w.double().cpu().numpy(), b.double().cpu().numpy())
+    np.testing.assert_allclose(lp.cpu().numpy(), O.token_logprobs(x, tok.cpu().numpy()), atol=ATOL)
+    np.testing.assert_allclose(ent.cpu().numpy(), O.token_entropy(x), atol=ATOL)
+
+
+def test_linear_logprob_fp16_no_bias_row_index():
+    h, w, _, tok_rows = _case(200, 5000, 192, dtype=torch.float16, bias=False, seed=5)
+    # rows map to a permuted global token order
+    perm = torch.randperm(200, device=DEV).to(torch.int32)
+    tokens = torch.empty(200, dtype=torch.int64, device=DEV)
+    tokens[perm.long()] = tok_rows
+    lp, _ = K.linear_logprob_fwd(h, w, tokens, row_index=perm)
+    rlp, _ = _ref(h, w, None, tok_rows, entropy=False)
+    torch.testing.assert_close(lp[perm.long()], rlp, rtol=0, atol=ATOL)
+
+
+def test_linear_logprob_matches_materialised_path():
+    # fused K7 == cuBLAS logits (fp32 out) + K1 on the same inputs
+    h, w, b, tok = _case(512, 32000, 512, seed=7)
+    lp, _ = K.linear_logprob_fwd(h, w, tok, bias=b)
+    logits = torch.addmm(b, h.float(), w.float().t())
+    lp1, _ = K.logprob_fwd(logits, tok, with_entropy=False)
+    torch.testing.assert_close(lp, lp1, rtol=0, atol=ATOL)
+
+
+def test_linear_logprob_rejects_bad_shapes():
+    h = torch.zeros(4, 100, dtype=torch.bfloat16, device=DEV)
+    w = torch.zeros(10, 100, dtype=torch.bfloat16, device=DEV)
+    t = torch.zeros(4, dtype=torch.int64, device=DEV)
+    with pytest.raises(RuntimeError):
+        K.linear_logprob_fwd(h, w, t)  # d % 64 != 0
+    with pytest.raises(TypeError):
+        K.linear_logprob_fwd(h.float(), w.float(), t)
