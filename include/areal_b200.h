@@ -186,13 +186,16 @@ int areal_fill_gather(const int64_t* traj_bounds, const int32_t* packed_traj,
  * row_index[r] (NULL = r): lp_out[idx] = x[tok] - logsumexp(x), entropy_out (may be
  * NULL) = -sum p log p, x = hidden[r] . weight^T + bias accumulated in fp32 on the
  * tensor cores.  The [n_rows, vocab] logits never reach HBM.  scratch (device) holds
- * per-(row, 2048-column block) partials: areal_linear_logprob_scratch_bytes(). */
+ * per-(row, 2048-column block) partials: areal_linear_logprob_scratch_bytes().
+ * cta_group: 1 = one CTA per 128-token tile (tcgen05 .cta_group::1, M=128),
+ * 2 = a CTA pair per 256-token tile (.cta_group::2, M=256, each CTA loads half of the
+ * W tile), 0 = choose (2 when n_rows > 128). */
 size_t areal_linear_logprob_scratch_bytes(int64_t n_rows, int64_t vocab);
 int areal_linear_logprob_fwd(const void* hidden, int64_t ld_hidden, const void* weight,
                              int64_t ld_weight, const float* bias, int dtype, int64_t n_rows,
                              int64_t vocab, int64_t dim, const int64_t* tokens,
                              const int32_t* row_index, double* lp_out, double* entropy_out,
-                             void* scratch, size_t scratch_bytes, void* stream);
+                             void* scratch, size_t scratch_bytes, int cta_group, void* stream);
 
 /* ---- K6: fused global-norm clip + Adam (decoupled weight decay), multi-tensor --
  * Replaces the optimizer step of train_step (trainer.py:329-331): grad.scale_(-1/n)

@@ -89,7 +89,8 @@ _SIGS = {
     "areal_fill_gather": ([c_vp, c_vp, c_vp, c_i32, c_i64, c_vp, c_vp, c_vp], ctypes.c_int),
     "areal_linear_logprob_scratch_bytes": ([c_i64, c_i64], c_sz),
     "areal_linear_logprob_fwd": ([c_vp, c_i64, c_vp, c_i64, c_vp, ctypes.c_int, c_i64, c_i64, c_i64,
-                                  c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp], ctypes.c_int),
+                                  c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, ctypes.c_int, c_vp],
+                                 ctypes.c_int),
     "areal_adam_step": ([ctypes.POINTER(AdamTensor), c_i32, ctypes.c_int, ctypes.c_int,
                          ctypes.POINTER(AdamParams), c_vp, c_vp, c_sz, c_vp], ctypes.c_int),
 }

@@ -34,14 +34,10 @@ constexpr int BM = 128;            // tokens per tile (TMEM lanes)
 constexpr int BN = 256;            // vocab columns per MMA / accumulator
 constexpr int BK = 64;             // k-slab: 64 x 2 B = one 128-byte swizzle row
 constexpr int UMMA_K = 16;         // K per tcgen05.mma for 16-bit inputs
-constexpr int STAGES = 4;
 constexpr int NT = 8;              // N-tiles per unit
 constexpr int VB = NT * BN;        // vocab block per unit
 constexpr int A_BYTES = BM * BK * 2;
-constexpr int B_BYTES = BN * BK * 2;
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int THREADS = 192;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024;  // + alignment slack for SW128
 
 struct Args {
   const float* bias;
@@ -107,100 +103,184 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ void tmem_ld32_issue(uint32_t taddr, float (&v)[32]) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, "
+      "%30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+template <int STAGES_>
 struct Pipe {
   uint32_t stage = 0, phase = 0;
   __device__ __forceinline__ void next() {
-    if (++stage == STAGES) {
+    if (++stage == STAGES_) {
       stage = 0;
       phase ^= 1u;
     }
   }
 };
 
-template <bool ENT>
+// Per-CTA-group geometry.  CG = 1: M = 128 per CTA, each CTA loads its A [128 x 64]
+// and the whole B [256 x 64] per k-slab (48 KB).  CG = 2 (CTA pair, tcgen05 .cta_group::2):
+// M = 256 over the pair, each CTA loads its A [128 x 64] and HALF of B [128 x 64]
+// (32 KB), the leader CTA issues the MMA that reads both CTAs' shared memory and writes
+// both CTAs' TMEM (each its 128 rows x 256 columns).
+template <int CG> struct Geo {
+  static constexpr int B_ROWS = BN / CG;                     // B rows loaded per CTA
+  static constexpr int STAGE = A_BYTES + B_ROWS * BK * 2;    // bytes per stage per CTA
+  static constexpr int NSTAGE = (CG == 1) ? 4 : 6;
+  static constexpr int SMEM = NSTAGE * STAGE + 1024;
+  static constexpr int TM = BM * CG;                         // tokens per unit
+};
+
+__device__ __forceinline__ void tma_load_2d_cg2(const CUtensorMap* map, void* smem_dst, uint32_t bar_cluster,
+                                                int32_t x, int32_t y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::
+          "r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void mma_bf16_cg2(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// commit to the barrier at the same offset in both CTAs of the pair
+__device__ __forceinline__ void mma_commit_cg2(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+template <int CG, bool ENT>
 __global__ void __launch_bounds__(THREADS, 1)
     linear_lp_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const Args a) {
+  using G = Geo<CG>;
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2];
+  __shared__ uint64_t full[G::NSTAGE], empty[G::NSTAGE], tfull[2], tempty[2];
   __shared__ uint32_t s_tbase;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ksteps = a.dim / BK;
+  const uint32_t rank = (CG == 2) ? cluster_ctarank() : 0u;
+  const int unit0 = (CG == 2) ? (int)cluster_id_x() : (int)blockIdx.x;
+  const int nunit_step = (CG == 2) ? (int)nclusters_x() : (int)gridDim.x;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < G::NSTAGE; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 4);  // one arrive per epilogue warp
+      mbar_init(&tempty[b], 4 * CG);  // one arrive per epilogue warp of the pair
     }
     fence_mbar_init_cluster();
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-                     smem_u32(&s_tbase))
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if constexpr (CG == 2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                       smem_u32(&s_tbase))
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                       smem_u32(&s_tbase))
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
     tc_fence_before();
   }
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync_all();  // peer barriers initialised before any remote use
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tbase = s_tbase;
 
   if (warp == 0) {
-    // ================= TMA producer
+    // ================= TMA producer (both CTAs; completion counted on the leader's barrier)
     if (lane == 0) {
-      Pipe p;
-      for (int u = blockIdx.x; u < a.n_units; u += gridDim.x) {
+      Pipe<G::NSTAGE> p;
+      for (int u = unit0; u < a.n_units; u += nunit_step) {
         const int mt = u % a.n_mt, vb = u / a.n_mt;
+        const int32_t arow = mt * G::TM + (int32_t)rank * BM;
         for (int n = 0; n < NT; ++n) {
           const int64_t n0 = (int64_t)vb * VB + (int64_t)n * BN;
           if (n0 >= a.vocab) break;
+          const int32_t brow = (int32_t)n0 + (int32_t)rank * G::B_ROWS;
           for (int ks = 0; ks < ksteps; ++ks) {
             mbar_wait(&empty[p.stage], p.phase ^ 1u);
-            unsigned char* st = smem + (size_t)p.stage * STAGE_BYTES;
-            mbar_arrive_expect_tx(&full[p.stage], STAGE_BYTES);
-            tma_load_2d(&tmA, st, &full[p.stage], ks * BK, mt * BM);
-            tma_load_2d(&tmB, st + A_BYTES, &full[p.stage], ks * BK, (int32_t)n0);
+            unsigned char* st = smem + (size_t)p.stage * G::STAGE;
+            if constexpr (CG == 2) {
+              const uint32_t bar0 = mapa_shared(smem_u32(&full[p.stage]), 0u);
+              if (rank == 0) mbar_arrive_expect_tx(&full[p.stage], 2 * G::STAGE);
+              tma_load_2d_cg2(&tmA, st, bar0, ks * BK, arow);
+              tma_load_2d_cg2(&tmB, st + A_BYTES, bar0, ks * BK, brow);
+            } else {
+              mbar_arrive_expect_tx(&full[p.stage], G::STAGE);
+              tma_load_2d(&tmA, st, &full[p.stage], ks * BK, arow);
+              tma_load_2d(&tmB, st + A_BYTES, &full[p.stage], ks * BK, brow);
+            }
             p.next();
           }
         }
       }
     }
   } else if (warp == 1) {
-    // ================= MMA issuer
-    if (lane == 0) {
-      Pipe p;
+    // ================= MMA issuer (leader CTA only for the pair)
+    if (lane == 0 && rank == 0) {
+      Pipe<G::NSTAGE> p;
       uint32_t acc = 0, acc_phase = 0;
-      for (int u = blockIdx.x; u < a.n_units; u += gridDim.x) {
+      for (int u = unit0; u < a.n_units; u += nunit_step) {
         const int vb = u / a.n_mt;
         for (int n = 0; n < NT; ++n) {
           const int64_t n0 = (int64_t)vb * VB + (int64_t)n * BN;
           if (n0 >= a.vocab) break;
-          mbar_wait(&tempty[acc], acc_phase ^ 1u);
+          if constexpr (CG == 2) mbar_wait_cluster(&tempty[acc], acc_phase ^ 1u);
+          else mbar_wait(&tempty[acc], acc_phase ^ 1u);
           tc_fence_after();
           const uint32_t d_tmem = tbase + acc * BN;
           for (int ks = 0; ks < ksteps; ++ks) {
             mbar_wait(&full[p.stage], p.phase);
             tc_fence_after();
-            const uint32_t sa = smem_u32(smem + (size_t)p.stage * STAGE_BYTES);
+            const uint32_t sa = smem_u32(smem + (size_t)p.stage * G::STAGE);
             const uint64_t adesc = sw128_desc(sa), bdesc = sw128_desc(sa + A_BYTES);
 #pragma unroll
             for (int kk = 0; kk < BK / UMMA_K; ++kk) {
               // advance the start address by kk * 32 bytes inside the swizzle row
-              mma_bf16(d_tmem, adesc + (uint64_t)(kk * 2), bdesc + (uint64_t)(kk * 2), a.idesc,
-                       (ks | kk) != 0);
+              if constexpr (CG == 2)
+                mma_bf16_cg2(d_tmem, adesc + (uint64_t)(kk * 2), bdesc + (uint64_t)(kk * 2), a.idesc,
+                             (ks | kk) != 0);
+              else
+                mma_bf16(d_tmem, adesc + (uint64_t)(kk * 2), bdesc + (uint64_t)(kk * 2), a.idesc,
+                         (ks | kk) != 0);
             }
-            mma_commit(&empty[p.stage]);  // frees the stage once these MMAs have read it
+            // frees the stage (in both CTAs) once these MMAs have read it
+            if constexpr (CG == 2) mma_commit_cg2(&empty[p.stage]);
+            else mma_commit(&empty[p.stage]);
             p.next();
           }
-          mma_commit(&tfull[acc]);  // accumulator complete -> epilogue
+          if constexpr (CG == 2) mma_commit_cg2(&tfull[acc]);  // accumulator complete -> epilogues
+          else mma_commit(&tfull[acc]);
           acc ^= 1u;
           if (acc == 0) acc_phase ^= 1u;
         }
@@ -208,14 +288,37 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   } else {
     // ================= epilogue: one thread per token row
+    // TMEM loads are double-buffered (chunk ch+1 in flight while ch is folded); the
+    // N-tile's 256 biases are staged in shared memory one N-tile ahead (one named
+    // barrier per N-tile among the 4 epilogue warps).
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int r_local = q * 32 + lane;
+    const int et = threadIdx.x - 64;  // 0..127
     const uint32_t lane_base = tbase + ((uint32_t)(q * 32) << 16);
-    uint32_t acc = 0, acc_phase = 0;
+    const uint32_t tempty0 = (CG == 2) ? mapa_shared(smem_u32(&tempty[0]), 0u) : 0u;
+    __shared__ __align__(16) float sbias[2][BN];
+    uint32_t acc = 0, acc_phase = 0, bpar = 0;
     constexpr float L2E = 1.4426950408889634f;
-    for (int u = blockIdx.x; u < a.n_units; u += gridDim.x) {
+    // iteration order of (unit, N-tile) pairs, identical to the producer / MMA loops
+    auto tile_n0 = [&](int u, int n) -> int64_t { return (int64_t)(u / a.n_mt) * VB + (int64_t)n * BN; };
+    auto load_bias = [&](int64_t n0) -> float2 {
+      float2 b2 = make_float2(0.f, 0.f);
+      if (a.bias != nullptr && n0 >= 0) {
+        const int64_t c = n0 + 2 * et;
+        if (c < a.vocab) b2.x = __ldg(a.bias + c);
+        if (c + 1 < a.vocab) b2.y = __ldg(a.bias + c + 1);
+      }
+      return b2;
+    };
+    if (unit0 < a.n_units) {
+      const float2 b2 = load_bias(tile_n0(unit0, 0));
+      sbias[0][2 * et] = b2.x;
+      sbias[0][2 * et + 1] = b2.y;
+    }
+    named_bar_sync(1, 128);
+    for (int u = unit0; u < a.n_units; u += nunit_step) {
       const int mt = u % a.n_mt, vb = u / a.n_mt;
-      const int64_t row = (int64_t)mt * BM + r_local;
+      const int64_t row = (int64_t)mt * G::TM + (int64_t)rank * BM + r_local;
       int64_t tok = -1;
       if (row < a.n_rows) {
         const int64_t idx = a.row_index ? (int64_t)a.row_index[row] : row;
@@ -223,45 +326,44 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       float m = -INFINITY, s = 0.f, sx = 0.f, xa = 0.f;
       for (int n = 0; n < NT; ++n) {
-        const int64_t n0 = (int64_t)vb * VB + (int64_t)n * BN;
+        const int64_t n0 = tile_n0(u, n);
         if (n0 >= a.vocab) break;
+        // prefetch the biases of the next (unit, N-tile) in iteration order
+        int64_t nn0 = -1;
+        if (n + 1 < NT && tile_n0(u, n + 1) < a.vocab) nn0 = tile_n0(u, n + 1);
+        else if (u + nunit_step < a.n_units) nn0 = tile_n0(u + nunit_step, 0);
+        const float2 bnext = load_bias(nn0);
+        const float* bs = sbias[bpar];
+
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
-#pragma unroll 1
-        for (int ch = 0; ch < BN / 32; ++ch) {
-          float v[32];
-          tmem_ld32(lane_base + acc * BN + ch * 32, v);
+        const uint32_t tcol = lane_base + acc * BN;
+        auto fold_chunk = [&](float(&cv)[32], int ch) {
           const int64_t c0 = n0 + ch * 32;
           if (a.bias != nullptr) {
-            const float4* b4 = reinterpret_cast<const float4*>(a.bias + c0);
+            const float4* b4 = reinterpret_cast<const float4*>(bs + ch * 32);
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-              if (c0 + 4 * i + 3 < a.vocab) {
-                const float4 bb = __ldg(b4 + i);
-                v[4 * i] += bb.x;
-                v[4 * i + 1] += bb.y;
-                v[4 * i + 2] += bb.z;
-                v[4 * i + 3] += bb.w;
-              } else {
-#pragma unroll
-                for (int e = 0; e < 4; ++e)
-                  if (c0 + 4 * i + e < a.vocab) v[4 * i + e] += __ldg(a.bias + c0 + 4 * i + e);
-              }
+              const float4 bb = b4[i];
+              cv[4 * i] += bb.x;
+              cv[4 * i + 1] += bb.y;
+              cv[4 * i + 2] += bb.z;
+              cv[4 * i + 3] += bb.w;
             }
           }
           if (c0 + 32 > a.vocab) {  // vocab tail: columns past V are padding
 #pragma unroll
             for (int i = 0; i < 32; ++i)
-              if (c0 + i >= a.vocab) v[i] = -INFINITY;
+              if (c0 + i >= a.vocab) cv[i] = -INFINITY;
           }
           if (tok >= c0 && tok < c0 + 32) {  // rare: the token's logit
 #pragma unroll
             for (int i = 0; i < 32; ++i)
-              if (c0 + i == tok) xa = v[i];
+              if (c0 + i == tok) xa = cv[i];
           }
-          float lmax = v[0];
+          float lmax = cv[0];
 #pragma unroll
-          for (int i = 1; i < 32; ++i) lmax = fmaxf(lmax, v[i]);
+          for (int i = 1; i < 32; ++i) lmax = fmaxf(lmax, cv[i]);
           const float mn = fmaxf(m, lmax);
           const float c = (mn == -INFINITY) ? 0.f : mn * L2E;
           const float r = fast_exp2(fmaf(m, L2E, -c));
@@ -269,7 +371,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           float2 s2 = make_float2(0.f, 0.f), x2 = make_float2(0.f, 0.f);
 #pragma unroll
           for (int i = 0; i < 32; i += 2) {
-            const float2 x = make_float2(v[i], v[i + 1]);
+            const float2 x = make_float2(cv[i], cv[i + 1]);
             const float2 t = ffma2(x, L2, C2);
             const float2 e = make_float2(fast_exp2(t.x), fast_exp2(t.y));
             s2 = fadd2(s2, e);
@@ -281,20 +383,45 @@ __global__ void __launch_bounds__(THREADS, 1)
           s = s * r + (s2.x + s2.y);
           if (ENT) sx = sx * r + (x2.x + x2.y);
           m = mn;
+        };
+        float va[32], vb[32];
+        tmem_ld32_issue(tcol, va);
+        tmem_ld_wait();
+#pragma unroll 1
+        for (int ch = 0; ch < BN / 32; ch += 2) {
+          tmem_ld32_issue(tcol + (ch + 1) * 32, vb);  // in flight while va is folded
+          fold_chunk(va, ch);
+          tmem_ld_wait();
+          if (ch + 2 < BN / 32) tmem_ld32_issue(tcol + (ch + 2) * 32, va);
+          fold_chunk(vb, ch + 1);
+          if (ch + 2 < BN / 32) tmem_ld_wait();
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (lane == 0) {
+          if constexpr (CG == 2)  // release this CTA's TMEM reads to the leader's MMA issuer
+            mbar_remote_arrive_release(tempty0 + acc * (uint32_t)sizeof(uint64_t));
+          else
+            mbar_arrive(&tempty[acc]);
+        }
         acc ^= 1u;
         if (acc == 0) acc_phase ^= 1u;
+        sbias[bpar ^ 1][2 * et] = bnext.x;
+        sbias[bpar ^ 1][2 * et + 1] = bnext.y;
+        bpar ^= 1u;
+        named_bar_sync(1, 128);
       }
       if (row < a.n_rows) a.partials[row * a.n_vb + vb] = make_float4(m, s, sx, xa);
     }
   }
   __syncthreads();
+  if constexpr (CG == 2) cluster_sync_all();  // both CTAs done with TMEM before the pair frees it
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tbase) : "memory");
+    if constexpr (CG == 2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tbase) : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tbase) : "memory");
   }
 }
 
@@ -366,7 +493,8 @@ extern "C" int areal_linear_logprob_fwd(const void* hidden, int64_t ld_hidden, c
                                         int64_t ld_weight, const float* bias, int dtype, int64_t n_rows,
                                         int64_t vocab, int64_t dim, const int64_t* tokens,
                                         const int32_t* row_index, double* lp_out, double* entropy_out,
-                                        void* scratch, size_t scratch_bytes, void* stream_) {
+                                        void* scratch, size_t scratch_bytes, int cta_group,
+                                        void* stream_) {
   using namespace areal::k7;
   if (n_rows < 0 || vocab < 1 || dim < 1) return AREAL_ERR_BAD_SHAPE;
   if (n_rows == 0) return AREAL_OK;
@@ -381,9 +509,6 @@ extern "C" int areal_linear_logprob_fwd(const void* hidden, int64_t ld_hidden, c
   if (!scratch || scratch_bytes < areal_linear_logprob_scratch_bytes(n_rows, vocab)) return AREAL_ERR_WORKSPACE;
   const CUtensorMapDataType dt = dtype == AREAL_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   CUtensorMap tmA, tmB;
-  if (!make_map(&tmA, hidden, dt, n_rows, dim, ld_hidden, BM) ||
-      !make_map(&tmB, weight, dt, vocab, dim, ld_weight, BN))
-    return AREAL_ERR_CUDA;
   Args a;
   a.bias = bias;
   a.tokens = tokens;
@@ -392,21 +517,47 @@ extern "C" int areal_linear_logprob_fwd(const void* hidden, int64_t ld_hidden, c
   a.n_rows = n_rows;
   a.vocab = vocab;
   a.dim = (int32_t)dim;
-  a.n_mt = (int32_t)((n_rows + BM - 1) / BM);
   a.n_vb = (int32_t)((vocab + VB - 1) / VB);
-  a.n_units = a.n_mt * a.n_vb;
   // kind::f16 instruction descriptor: D fp32, A/B bf16 (1) or fp16 (0), both K-major,
   // N >> 3 at bit 17, M >> 4 at bit 24 (cute::UMMA::InstrDescriptor)
   const uint32_t ab = dtype == AREAL_BF16 ? 1u : 0u;
-  a.idesc = (1u << 4) | (ab << 7) | (ab << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
   cudaStream_t stream = static_cast<cudaStream_t>(stream_);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int grid = std::min(sms, a.n_units);
-  auto kern = entropy_out ? linear_lp_kernel<true> : linear_lp_kernel<false>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-  kern<<<grid, THREADS, SMEM_BYTES, stream>>>(tmA, tmB, a);
+  // the CTA pair needs at least two token tiles' worth of rows to pay off
+  const int cg = (cta_group == 1 || cta_group == 2) ? cta_group : (n_rows > BM ? 2 : 1);
+  const int tm = BM * cg;
+  a.n_mt = (int32_t)((n_rows + tm - 1) / tm);
+  a.n_units = a.n_mt * a.n_vb;
+  a.idesc = (1u << 4) | (ab << 7) | (ab << 10) | ((uint32_t)(BN >> 3) << 17) |
+            ((uint32_t)((BM * cg) >> 4) << 24);
+  if (!make_map(&tmA, hidden, dt, n_rows, dim, ld_hidden, BM) ||
+      !make_map(&tmB, weight, dt, vocab, dim, ld_weight, BN / cg))
+    return AREAL_ERR_CUDA;
+  if (cg == 1) {
+    const int grid = std::min(sms, a.n_units);
+    auto kern = entropy_out ? linear_lp_kernel<1, true> : linear_lp_kernel<1, false>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo<1>::SMEM);
+    kern<<<grid, THREADS, Geo<1>::SMEM, stream>>>(tmA, tmB, a);
+  } else {
+    const int clusters = std::min(sms / 2, a.n_units);
+    auto kern = entropy_out ? linear_lp_kernel<2, true> : linear_lp_kernel<2, false>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo<2>::SMEM);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * clusters);
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = Geo<2>::SMEM;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, kern, tmA, tmB, a) != cudaSuccess) return AREAL_ERR_CUDA;
+  }
   AREAL_CUDA_CHECK_LAUNCH();
   const int64_t threads = n_rows * 32;
   linear_lp_merge_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, stream>>>(

@@ -327,7 +327,8 @@ def _scratch(dev, nbytes):
 
 def linear_logprob_fwd(hidden: torch.Tensor, weight: torch.Tensor, tokens: torch.Tensor,
                        bias: torch.Tensor | None = None, row_index: torch.Tensor | None = None,
-                       lp_out=None, entropy_out=None, with_entropy: bool = False):
+                       lp_out=None, entropy_out=None, with_entropy: bool = False,
+                       cta_group: int = 0):
     """Fused LM head + log-softmax-gather (K7, tcgen05): lp[idx] = log_softmax(h W^T + b)[tok].
 
     ``hidden`` [n, d] and ``weight`` [V, d] are bf16/fp16 (row-contiguous, d % 64 == 0),
@@ -362,6 +363,6 @@ def linear_logprob_fwd(hidden: torch.Tensor, weight: torch.Tensor, tokens: torch
     check(lib.areal_linear_logprob_fwd(_ptr(hidden), ld_h, _ptr(weight), ld_w, _ptr(bias),
                                        _lib.DTYPE_CODES[hidden.dtype], n, V, d, _ptr(tokens),
                                        _ptr(row_index), _ptr(lp_out), _ptr(entropy_out),
-                                       _ptr(scratch), scratch.numel(), _stream()),
+                                       _ptr(scratch), scratch.numel(), int(cta_group), _stream()),
           "areal_linear_logprob_fwd")
     return lp_out, entropy_out

@@ -40,11 +40,13 @@ def _ref(h, w, b, tok, entropy=True):
     return lp, ent
 
 
+@pytest.mark.parametrize("cg", [1, 2])
 @pytest.mark.parametrize("n,V,d", [(1, 1000, 64), (100, 4096, 128), (300, 32000, 256),
-                                   (129, 2049, 64), (257, 151936, 1536), (64, 152064, 512)])
-def test_linear_logprob_matches_float64(n, V, d):
+                                   (129, 2049, 64), (257, 151936, 1536), (64, 152064, 512),
+                                   (1000, 2000, 64)])
+def test_linear_logprob_matches_float64(n, V, d, cg):
     h, w, b, tok = _case(n, V, d)
-    lp, ent = K.linear_logprob_fwd(h, w, tok, bias=b, with_entropy=True)
+    lp, ent = K.linear_logprob_fwd(h, w, tok, bias=b, with_entropy=True, cta_group=cg)
     rlp, rent = _ref(h, w, b, tok)
     torch.testing.assert_close(lp, rlp, rtol=0, atol=ATOL)
     torch.testing.assert_close(ent, rent, rtol=1e-5, atol=ATOL)
@@ -59,13 +61,14 @@ def test_linear_logprob_numpy_oracle_small():
     np.testing.assert_allclose(ent.cpu().numpy(), O.token_entropy(x), atol=ATOL)
 
 
-def test_linear_logprob_fp16_no_bias_row_index():
+@pytest.mark.parametrize("cg", [1, 2])
+def test_linear_logprob_fp16_no_bias_row_index(cg):
     h, w, _, tok_rows = _case(200, 5000, 192, dtype=torch.float16, bias=False, seed=5)
     # rows map to a permuted global token order
     perm = torch.randperm(200, device=DEV).to(torch.int32)
     tokens = torch.empty(200, dtype=torch.int64, device=DEV)
     tokens[perm.long()] = tok_rows
-    lp, _ = K.linear_logprob_fwd(h, w, tokens, row_index=perm)
+    lp, _ = K.linear_logprob_fwd(h, w, tokens, row_index=perm, cta_group=cg)
     rlp, _ = _ref(h, w, None, tok_rows, entropy=False)
     torch.testing.assert_close(lp[perm.long()], rlp, rtol=0, atol=ATOL)
 

@@ -11,6 +11,7 @@ ap.add_argument("--vocab", type=int, default=151936)
 ap.add_argument("--dim", type=int, default=1536)
 ap.add_argument("--iters", type=int, default=10)
 ap.add_argument("--which", default="fused,unfused")
+ap.add_argument("--cg", type=int, default=0)
 a = ap.parse_args()
 dev = torch.device("cuda", 0)
 T, V, d = a.rows, a.vocab, a.dim
@@ -37,7 +38,7 @@ def timeit(fn):
 
 for which in a.which.split(","):
     if which == "fused":
-        ms = timeit(lambda: K.linear_logprob_fwd(h, w, tok, bias=b, lp_out=lp))
+        ms = timeit(lambda: K.linear_logprob_fwd(h, w, tok, bias=b, lp_out=lp, cta_group=a.cg))
     elif which == "gemm":
         ms = timeit(lambda: torch.addmm(b.to(torch.bfloat16), h, w.t()))
     else:
