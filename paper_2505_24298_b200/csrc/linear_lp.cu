@@ -37,7 +37,11 @@ constexpr int UMMA_K = 16;         // K per tcgen05.mma for 16-bit inputs
 constexpr int NT = 8;              // N-tiles per unit
 constexpr int VB = NT * BN;        // vocab block per unit
 constexpr int A_BYTES = BM * BK * 2;
-constexpr int THREADS = 192;
+constexpr int EPI_SPLIT = 2;       // epilogue warps per TMEM lane quarter (column halves)
+constexpr int EPI_THREADS = 128 * EPI_SPLIT;
+constexpr int THREADS = 64 + EPI_THREADS;
+constexpr int CH_PER_WARP = BN / 32 / EPI_SPLIT;  // 32-column chunks per epilogue warp per N-tile
+static_assert(EPI_THREADS == BN, "bias staging: one bias per epilogue thread per N-tile");
 
 struct Args {
   const float* bias;
@@ -191,7 +195,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 4 * CG);  // one arrive per epilogue warp of the pair
+      mbar_init(&tempty[b], 4 * EPI_SPLIT * CG);  // one arrive per epilogue warp of the pair
     }
     fence_mbar_init_cluster();
     prefetch_tmap(&tmA);
@@ -293,7 +297,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     // barrier per N-tile among the 4 epilogue warps).
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int r_local = q * 32 + lane;
-    const int et = threadIdx.x - 64;  // 0..127
+    const int et = threadIdx.x - 64;  // 0..EPI_THREADS-1
+    const int half = (warp - 2) >> 2;  // which column slice of each N-tile this warp folds
     const uint32_t lane_base = tbase + ((uint32_t)(q * 32) << 16);
     const uint32_t tempty0 = (CG == 2) ? mapa_shared(smem_u32(&tempty[0]), 0u) : 0u;
     __shared__ __align__(16) float sbias[2][BN];
@@ -304,18 +309,16 @@ __global__ void __launch_bounds__(THREADS, 1)
     auto load_bias = [&](int64_t n0) -> float2 {
       float2 b2 = make_float2(0.f, 0.f);
       if (a.bias != nullptr && n0 >= 0) {
-        const int64_t c = n0 + 2 * et;
+        const int64_t c = n0 + et;
         if (c < a.vocab) b2.x = __ldg(a.bias + c);
-        if (c + 1 < a.vocab) b2.y = __ldg(a.bias + c + 1);
       }
       return b2;
     };
     if (unit0 < a.n_units) {
       const float2 b2 = load_bias(tile_n0(unit0, 0));
-      sbias[0][2 * et] = b2.x;
-      sbias[0][2 * et + 1] = b2.y;
+      sbias[0][et] = b2.x;
     }
-    named_bar_sync(1, 128);
+    named_bar_sync(1, EPI_THREADS);
     for (int u = unit0; u < a.n_units; u += nunit_step) {
       const int mt = u % a.n_mt, vb = u / a.n_mt;
       const int64_t row = (int64_t)mt * G::TM + (int64_t)rank * BM + r_local;
@@ -385,16 +388,17 @@ __global__ void __launch_bounds__(THREADS, 1)
           m = mn;
         };
         float va[32], vb[32];
-        tmem_ld32_issue(tcol, va);
+        const int ch0 = half * CH_PER_WARP;
+        tmem_ld32_issue(tcol + ch0 * 32, va);
         tmem_ld_wait();
 #pragma unroll 1
-        for (int ch = 0; ch < BN / 32; ch += 2) {
+        for (int ch = ch0; ch < ch0 + CH_PER_WARP; ch += 2) {
           tmem_ld32_issue(tcol + (ch + 1) * 32, vb);  // in flight while va is folded
           fold_chunk(va, ch);
           tmem_ld_wait();
-          if (ch + 2 < BN / 32) tmem_ld32_issue(tcol + (ch + 2) * 32, va);
+          if (ch + 2 < ch0 + CH_PER_WARP) tmem_ld32_issue(tcol + (ch + 2) * 32, va);
           fold_chunk(vb, ch + 1);
-          if (ch + 2 < BN / 32) tmem_ld_wait();
+          if (ch + 2 < ch0 + CH_PER_WARP) tmem_ld_wait();
         }
         tc_fence_before();
         __syncwarp();
@@ -406,12 +410,11 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         acc ^= 1u;
         if (acc == 0) acc_phase ^= 1u;
-        sbias[bpar ^ 1][2 * et] = bnext.x;
-        sbias[bpar ^ 1][2 * et + 1] = bnext.y;
+        sbias[bpar ^ 1][et] = bnext.x;
         bpar ^= 1u;
-        named_bar_sync(1, 128);
+        named_bar_sync(1, EPI_THREADS);
       }
-      if (row < a.n_rows) a.partials[row * a.n_vb + vb] = make_float4(m, s, sx, xa);
+      if (row < a.n_rows) a.partials[(row * a.n_vb + vb) * EPI_SPLIT + half] = make_float4(m, s, sx, xa);
     }
   }
   __syncthreads();
@@ -434,8 +437,8 @@ __global__ void linear_lp_merge_kernel(const float4* partials, int n_vb, int64_t
   if (row >= n_rows) return;
   RowStat<float> w;
   w.init();
-  for (int j = lane; j < n_vb; j += 32) {
-    const float4 p = partials[row * n_vb + j];
+  for (int j = lane; j < n_vb * EPI_SPLIT; j += 32) {
+    const float4 p = partials[row * n_vb * EPI_SPLIT + j];
     w.merge(p.x, p.y, p.z);
   }
   // fixed-order butterfly: identical on every lane, deterministic
@@ -445,7 +448,8 @@ __global__ void linear_lp_merge_kernel(const float4* partials, int n_vb, int64_t
     const int64_t tok = tokens[idx];
     const double lse = (double)w.m + log((double)w.s);
     double xa = nan("");
-    if (tok >= 0 && tok < vocab) xa = (double)partials[row * n_vb + tok / VB].w;
+    if (tok >= 0 && tok < vocab)  // the partial of the (block, column slice) holding the token
+      xa = (double)partials[(row * n_vb + tok / VB) * EPI_SPLIT + (int)((tok % BN) / (BN / EPI_SPLIT))].w;
     lp[idx] = xa - lse;
     if (ent) ent[idx] = lse - (double)w.sx / (double)w.s;
   }
@@ -486,7 +490,7 @@ using namespace areal;
 
 extern "C" size_t areal_linear_logprob_scratch_bytes(int64_t n_rows, int64_t vocab) {
   const int64_t n_vb = (vocab + k7::VB - 1) / k7::VB;
-  return (size_t)(n_rows > 0 ? n_rows : 0) * (size_t)n_vb * sizeof(float4);
+  return (size_t)(n_rows > 0 ? n_rows : 0) * (size_t)n_vb * k7::EPI_SPLIT * sizeof(float4);
 }
 
 extern "C" int areal_linear_logprob_fwd(const void* hidden, int64_t ld_hidden, const void* weight,
