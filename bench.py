@@ -39,14 +39,14 @@ CONFIGS = {
     # BASELINE.json configs[1]: the headline single-GPU workload
     "cfg2": dict(workload="Qwen2-1.5B shape (BASELINE configs[1])", vocab=151936, rollouts=512,
                  prompts=128, len_lo=128, len_hi=8192, dtype="bf16", budget=32768,
-                 minibatches=4),
+                 minibatches=4, hidden=1536),
     # configs[0]: CPU-reference synthetic case
     "cfg1": dict(workload="CPU-ref synthetic (BASELINE configs[0])", vocab=32000, rollouts=64,
                  prompts=16, len_lo=128, len_hi=2048, dtype="fp32", budget=32768, minibatches=4),
     # configs[2]: Qwen2-7B shape, eta=4 staleness mask
     "cfg3": dict(workload="Qwen2-7B shape (BASELINE configs[2])", vocab=152064, rollouts=1024,
                  prompts=256, len_lo=128, len_hi=27648, dtype="bf16", budget=32768,
-                 minibatches=4, eta=4),
+                 minibatches=4, eta=4, hidden=3584),
     # configs[3]: GRPO group-normalised advantages, 16 samples/prompt, versions lag 0..8
     "cfg4": dict(workload="GRPO 16 samples/prompt, mixed versions (BASELINE configs[3])",
                  vocab=151936, rollouts=1024, prompts=64, len_lo=128, len_hi=8192, dtype="bf16",
@@ -65,6 +65,60 @@ def _peaks():
         return float(p["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
     except Exception:
         return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+def _tensor_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["bf16_tflops"]), float(p.get("bf16_tflops_sustained", 0.0)) or None, \
+            "MEASURED_PEAKS.json bf16_tflops (cuBLAS 8192^3 burst)"
+    except Exception:
+        return 2250.0, None, "nominal 2.25 PFLOP/s dense bf16"
+
+
+def fused_head_bench(cfg, dev, iters=5):
+    """Auxiliary measurement of K7: the prox pass with the model's
+    LM head fused in (hidden [C, d] x W [V, d] -> log-probs, no [C, V] logits), on one
+    full micro-batch of the config's shape, against the materialised path (cuBLAS
+    bf16 GEMM -> bf16 logits -> K1).  Random hidden states / head weights."""
+    import torch
+    from paper_2505_24298_b200 import kernels as K
+    C, V, d = cfg["budget"], cfg["vocab"], cfg["hidden"]
+    g = torch.Generator(device=dev).manual_seed(11)
+    h = torch.randn(C, d, device=dev, generator=g).to(torch.bfloat16)
+    w = (torch.randn(V, d, device=dev, generator=g) / d ** 0.5 * 4).to(torch.bfloat16)
+    b = torch.randn(V, device=dev, generator=g)
+    tok = torch.randint(0, V, (C,), device=dev, generator=g)
+    lp = torch.empty(C, dtype=torch.float64, device=dev)
+    bb = b.to(torch.bfloat16)
+
+    def t(fn):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(iters):
+            fn()
+        e.record()
+        torch.cuda.synchronize()
+        return s.elapsed_time(e) / iters
+
+    fused = t(lambda: K.linear_logprob_fwd(h, w, tok, bias=b, lp_out=lp))
+
+    def unfused():
+        K.logprob_fwd(torch.addmm(bb, h, w.t()), tok, lp_out=lp, with_entropy=False)
+    base = t(unfused)
+    flop = 2.0 * C * V * d
+    peak, sustained, src = _tensor_peak()
+    tf = flop / (fused * 1e-3) / 1e12
+    return dict(kernel="areal_linear_logprob_fwd (K7, tcgen05 cta_group::2)", tokens=C, vocab=V,
+                hidden=d, ms=fused, tokens_per_s=C / (fused * 1e-3), tflops=tf,
+                frac_of_peak=tf / peak, peak_tflops=peak, peak_source=src,
+                frac_of_sustained=(tf / sustained) if sustained else None,
+                unfused_ms=base, unfused="cuBLAS bf16 GEMM -> bf16 logits -> K1",
+                speedup_vs_unfused=base / fused)
 
 
 def workload_arrays(cfg, n_copies=1, seed=0):
@@ -352,12 +406,17 @@ def run_ours(args, cfg):
         peak, peak_src = _peaks()
         k2_gbs = (k2_bytes / (k2_ms * 1e-3)) / 1e9 if k2_ms > 0 else 0.0
         k1_gbs = (k1_bytes / (k1_ms * 1e-3)) / 1e9 if k1_ms > 0 else 0.0
+        # DRAM bytes per token of K2 from the committed ncu --set full capture, scaled
+        # to this run's average launch
         traffic = None
         tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tp):
             try:
                 with open(tp) as f:
-                    traffic = json.load(f).get("k2_dram_bytes_per_launch")
+                    tj = json.load(f)
+                key = f"k2_{cfg['dtype']}_V{V}_dram_bytes_per_token"
+                if key in tj and n_k2:
+                    traffic = tj[key] * (k2_bytes / (2 * V * (2 if ldt == torch.bfloat16 else 4) + 52)) / n_k2
             except Exception:
                 traffic = None
         es = 2 if ldt == torch.bfloat16 else 4
@@ -373,7 +432,8 @@ def run_ours(args, cfg):
                         l2="inputs > L2: %d rotating %.1f GB logits buffers" % (
                             n_buf, C * V * es / 1e9),
                         parallelism=f"dp{world}", micro_batches=res.microbatches),
-            roofline=dict(bound="hbm", kernel="areal_ppo_fwd_bwd (K2, row_ring)",
+            roofline=dict(bound="hbm", kernel="areal_ppo_fwd_bwd (K2, %s)" % (
+                              "ppo_tmem_kernel" if V * es > 220 * 1024 else "ppo_ring_kernel"),
                           achieved=k2_gbs, peak=peak, unit="GB/s", frac=k2_gbs / peak,
                           traffic=traffic, peak_source=peak_src,
                           algorithmic_bytes_per_token=2 * V * es + 52,
@@ -391,6 +451,8 @@ def run_ours(args, cfg):
             cpu_baseline=cpu_base,
             loss=res.loss, clip_fraction=res.clip_fraction,
         )
+        if world == 1 and "hidden" in cfg and not args.no_fused_head:
+            line["fused_head"] = fused_head_bench(cfg, dev)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -409,6 +471,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-seconds", type=float, default=6.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-fused-head", action="store_true",
+                    help="skip the auxiliary K7 fused LM-head measurement")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     ap.add_argument("--share-gpu", action="store_true",
                     help="all ranks on cuda:0 (functional multi-rank check on one GPU)")

@@ -9,6 +9,10 @@ callbacks, so this module owns exactly the hot path and nothing else.
         phase 'prox'  : forward under the params at batch arrival (K1 consumes it)
         phase 'train' : forward under the current params (K2 consumes it)
         rows          : int32 CUDA tensor, global token index of each packed row
+    prox_head_fn(minibatch, micro, rows) -> (hidden [len(rows), d], W [V, d], bias|None)
+        optional replacement of logits_fn for the 'prox' phase: the model hands over
+        its final hidden states and LM head and K7 (tcgen05) computes the prox
+        log-probs without materialising the [rows, V] logits
     backward_fn(minibatch, micro, dlogits)   -> model backward from dlogits (optional)
     update_fn(minibatch, stats)              -> optimizer step; stats is the
         all-reduced float64[8] device tensor of the minibatch, so the caller
@@ -191,6 +195,7 @@ class DecoupledPPOStep:
         self.k2_events: list = []
         self.k2_bytes = 0
         self.k1_bytes = 0
+        self.k7_flops = 0
         self.record_events = False
 
     # ---- K3
@@ -243,14 +248,22 @@ class DecoupledPPOStep:
         events.append((s, e))
         return out
 
-    # ---- K1 over this rank's micro-batches (prox, once per global batch)
-    def prox_logprobs(self, ro: PackedRollouts, sp: StepPlan, logits_fn) -> torch.Tensor:
+    # ---- K1 (or fused K7) over this rank's micro-batches (prox, once per global batch)
+    def prox_logprobs(self, ro: PackedRollouts, sp: StepPlan, logits_fn=None,
+                      head_fn=None) -> torch.Tensor:
         # zeros: under DP each token's prox is written by exactly one rank, so a SUM
         # all-reduce (if a caller needs the full vector) reconstructs it
         prox = torch.zeros(ro.n_tokens, dtype=torch.float64, device=self.device)
         for m, groups in enumerate(sp.mine):
             for g, lo, hi in groups:
                 rows = sp.gather[lo:hi]
+                if head_fn is not None:  # trainer.py:128-137 with the output layer fused in
+                    hidden, weight, bias = head_fn(m, g, rows)
+                    self._timed(self.k1_events, lambda: K.linear_logprob_fwd(
+                        hidden, weight, ro.tokens, bias=bias, row_index=rows, lp_out=prox))
+                    self.k7_flops += 2 * (hi - lo) * weight.shape[0] * weight.shape[1]
+                    self.launches += 2
+                    continue
                 logits = logits_fn("prox", m, g, rows)
                 self._timed(self.k1_events, lambda: K.logprob_fwd(
                     logits, ro.tokens, row_index=rows, lp_out=prox, with_entropy=False,
@@ -261,11 +274,11 @@ class DecoupledPPOStep:
 
     # ---- full step
     def run(self, ro: PackedRollouts, logits_fn, backward_fn=None, update_fn=None,
-            current_version: int = 0, dlogits_fn=None) -> StepResult:
+            current_version: int = 0, dlogits_fn=None, prox_head_fn=None) -> StepResult:
         c = self.cfg
         adv = self.advantages(ro)                               # trainer.py:296
         sp = self.plan(ro)                                      # 300-315
-        prox = self.prox_logprobs(ro, sp, logits_fn)            # 295 (before any update)
+        prox = self.prox_logprobs(ro, sp, logits_fn, prox_head_fn)  # 295 (before any update)
         decoupled = c.objective == "decoupled"
         M = len(sp.items)
         mstats = torch.zeros((max(M, 1), K._lib.N_STATS), dtype=torch.float64, device=self.device)
@@ -298,3 +311,22 @@ class DecoupledPPOStep:
                           minibatch_updates=M, microbatches=micro_count,
                           excluded_tokens=int(tot[4]), masked_tokens=int(tot[5]),
                           entropy=float(tot[6]) / d, minibatch_stats=s)
+
+
+def emission_logprobs(tokens: torch.Tensor, logits: torch.Tensor | None = None,
+                      hidden: torch.Tensor | None = None, weight: torch.Tensor | None = None,
+                      bias: torch.Tensor | None = None) -> torch.Tensor:
+    """Behaviour log-probs recorded at emission (rollout.py:154-159: ``P.log_prob``
+    of each sampled token under the generating params), for one decode step of a
+    batch of sequences.  Either the step's logits [B, V] (K1) or the final hidden
+    states [B, d] + LM head [V, d] (+ bias) (K7, no logits) are given.  Returns
+    float64 [B] — the ``behavior_logprobs`` entries appended to each trajectory."""
+    if (logits is None) == (hidden is None):
+        raise ValueError("pass exactly one of logits or hidden (+ weight)")
+    if logits is not None:
+        lp, _ = K.logprob_fwd(logits, tokens, with_entropy=False)
+        return lp
+    if weight is None:
+        raise ValueError("hidden needs the LM-head weight")
+    lp, _ = K.linear_logprob_fwd(hidden, weight, tokens, bias=bias)
+    return lp

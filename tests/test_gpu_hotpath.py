@@ -80,3 +80,50 @@ def test_run_rejects_oversized_sequences():
     with pytest.raises(BatchError, match="exceeds capacity"):
         DecoupledPPOStep(HotPathConfig(micro_token_budget=40)).run(
             ro, lambda *a: None)
+
+
+def test_run_with_fused_head_prox_matches_logits_path():
+    # prox through K7 (hidden states + LM head, no logits) == prox through K1 on the
+    # materialised fp32 logits of the same head
+    rng = np.random.default_rng(4)
+    lengths = rng.integers(20, 400, size=24)
+    bounds = np.concatenate([[0], np.cumsum(lengths)]).astype(np.int64)
+    T, V, d = int(bounds[-1]), 3000, 128
+    g = torch.Generator(device="cuda").manual_seed(4)
+    H = torch.randn(T, d, device="cuda", generator=g).to(torch.bfloat16)
+    W = (torch.randn(V, d, device="cuda", generator=g) / d ** 0.5 * 3).to(torch.bfloat16)
+    b = torch.randn(V, device="cuda", generator=g)
+    table = torch.addmm(b, H.float(), W.float().t())  # fp32 logits of the same head
+    tokens = rng.integers(0, V, size=T)
+    behav = rng.normal(-8, 0.3, size=T)
+    rewards = rng.choice([5.0, -5.0], size=24)
+    ro = PackedRollouts.from_host(bounds, tokens, behav, rewards)
+    cfg = HotPathConfig(minibatches=2, micro_token_budget=1500)
+    outs = []
+    for fused in (False, True):
+        runner = DecoupledPPOStep(cfg)
+        sp = runner.plan(ro)
+        if fused:
+            prox = runner.prox_logprobs(ro, sp, head_fn=lambda m, g_, rows: (
+                H.index_select(0, rows.long()), W, b))
+        else:
+            prox = runner.prox_logprobs(ro, sp, lambda ph, m, g_, rows: table.index_select(0, rows.long()))
+        outs.append(prox)
+    torch.testing.assert_close(outs[1], outs[0], rtol=0, atol=2e-4)
+
+
+def test_emission_logprobs_k1_and_k7():
+    from paper_2505_24298_b200.hotpath import emission_logprobs
+    g = torch.Generator(device="cuda").manual_seed(9)
+    B, V, d = 64, 5000, 256
+    H = torch.randn(B, d, device="cuda", generator=g).to(torch.bfloat16)
+    W = (torch.randn(V, d, device="cuda", generator=g) / 8).to(torch.bfloat16)
+    tok = torch.randint(0, V, (B,), device="cuda", generator=g)
+    x = H.double() @ W.double().t()
+    ref = O.token_logprobs(x.cpu().numpy(), tok.cpu().numpy())
+    lp7 = emission_logprobs(tok, hidden=H, weight=W)
+    lp1 = emission_logprobs(tok, logits=x.float())
+    np.testing.assert_allclose(lp7.cpu().numpy(), ref, atol=2e-4)
+    np.testing.assert_allclose(lp1.cpu().numpy(), ref, atol=1e-4)
+    with pytest.raises(ValueError):
+        emission_logprobs(tok)

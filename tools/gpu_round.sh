@@ -14,9 +14,9 @@ for d in bf16 f32; do
   timeout 300 python tools/kbench.py --rows 32768 --vocab $V --dtype $d >> $O/${TAG}_kbench.jsonl 2>>$O/${TAG}_kbench.err
 done
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
-  --log-file $O/${TAG}_launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > $O/${TAG}_ncu_bench.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:logprob_ring -c 1 \
+  --log-file $O/${TAG}_launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-fused-head > $O/${TAG}_ncu_bench.log 2>&1
+[ -n "$FULL" ] && timeout 600 ncu --set full --clock-control none --import-source on -k regex:logprob_ring -c 1 \
   -o $O/${TAG}_k1 -f python tools/kbench.py --rows 8192 --which k1 --iters 1 > $O/${TAG}_ncu_k1.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:ppo_ -c 1 \
+[ -n "$FULL" ] && timeout 600 ncu --set full --clock-control none --import-source on -k regex:ppo_ -c 1 \
   -o $O/${TAG}_k2 -f python tools/kbench.py --rows 8192 --which k2 --iters 1 > $O/${TAG}_ncu_k2.log 2>&1
 ls -la $O
