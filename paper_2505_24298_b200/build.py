@@ -33,13 +33,40 @@ def _stale() -> bool:
     if not os.path.exists(LIB_PATH):
         return True
     t = os.path.getmtime(LIB_PATH)
-    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
+    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if not f.endswith(".c")]
     deps.append(os.path.join(ROOT, "include", "areal_b200.h"))
     deps.append(os.path.abspath(__file__))
     return any(os.path.getmtime(p) > t for p in deps)
 
 
+PACKER_SRC = os.path.join(CSRC, "packer.c")
+
+
+def packer_path() -> str:
+    import sysconfig
+    return os.path.join(HERE, "_packer" + sysconfig.get_config_var("EXT_SUFFIX"))
+
+
+def build_packer(force: bool = False) -> str:
+    """gcc -> the CPython extension _packer (host-side rollout packing, no CUDA)."""
+    import sysconfig
+    out = packer_path()
+    if not force and os.path.exists(out) and os.path.getmtime(out) >= os.path.getmtime(PACKER_SRC):
+        return out
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        raise RuntimeError("gcc not found; needed for the native rollout packer")
+    cmd = [cc, "-O3", "-shared", "-fPIC", "-Wall", "-Wno-unused-label",
+           "-I", sysconfig.get_paths()["include"], PACKER_SRC, "-o", out + ".tmp"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"gcc failed:\n{' '.join(cmd)}\n{res.stdout}\n{res.stderr}")
+    os.replace(out + ".tmp", out)
+    return out
+
+
 def build(verbose: bool = False, force: bool = False, extra_flags=()) -> str:
+    build_packer(force=force)
     if not force and not _stale():
         return LIB_PATH
     cmd = [nvcc_path(), *ARCH, "-O3", "-std=c++17", "-lineinfo", "--expt-relaxed-constexpr",

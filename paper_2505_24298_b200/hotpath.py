@@ -115,6 +115,50 @@ class PackedRollouts:
                               up(values, torch.float64))
 
 
+def _packer():
+    try:
+        from . import _packer as P  # built by paper_2505_24298_b200.build (gcc)
+    except ImportError as e:
+        raise ImportError("the native rollout packer is not built: run "
+                          "`python -m paper_2505_24298_b200.build`") from e
+    return P
+
+
+def pack_trajectories(trajectories, device=None, pin: bool = True, with_groups: bool = True):
+    """Replay-buffer trajectories (formation order) -> PackedRollouts on the GPU.
+
+    build_train_batch (trainer.py:83-111) without the per-token Python loop: the
+    native packer (csrc/packer.c) writes tokens / behaviour log-probs / per-token
+    versions / cu_seqlens / rewards straight into pinned host tensors, which are
+    copied to the device asynchronously on the current stream.  GRPO group ids are
+    the dense ids of ``traj.prompt.id`` in first-appearance order (tasks.py:80, the
+    harness's n_prompts x n_responses batch, harness.py:93-95).  Returns
+    (PackedRollouts, host tensors) — keep the host tensors alive until the copies
+    have completed (e.g. reuse them for the next batch).
+    """
+    P = _packer()
+    trajs = list(trajectories)
+    T, n = P.count(trajs)
+    alloc = (lambda *a, **k: torch.empty(*a, **k).pin_memory()) if pin else torch.empty
+    host = dict(tokens=alloc(T, dtype=torch.int64), behav=alloc(T, dtype=torch.float64),
+                versions=alloc(T, dtype=torch.int32), traj_bounds=alloc(n + 1, dtype=torch.int64),
+                rewards=alloc(n, dtype=torch.float64))
+    have_versions = P.fill(trajs, host["tokens"].data_ptr(), host["behav"].data_ptr(),
+                           host["versions"].data_ptr(), host["traj_bounds"].data_ptr(),
+                           host["rewards"].data_ptr(), T)
+    if not have_versions:
+        host["versions"] = None
+    if with_groups:
+        ids: dict = {}
+        g = [ids.setdefault(getattr(getattr(t, "prompt", None), "id", k), len(ids))
+             for k, t in enumerate(trajs)]
+        host["group_ids"] = torch.tensor(g, dtype=torch.int32)
+        if pin:
+            host["group_ids"] = host["group_ids"].pin_memory()
+    ro = PackedRollouts.from_host(**host, device=device)
+    return ro, host
+
+
 @dataclass
 class StepPlan:
     """Output of K4/K5 for one global batch plus this rank's share."""

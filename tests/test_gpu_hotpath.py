@@ -127,3 +127,25 @@ def test_emission_logprobs_k1_and_k7():
     np.testing.assert_allclose(lp1.cpu().numpy(), ref, atol=1e-4)
     with pytest.raises(ValueError):
         emission_logprobs(tok)
+
+
+def test_pack_trajectories_to_device():
+    from types import SimpleNamespace
+    from paper_2505_24298_b200.hotpath import pack_trajectories
+    rng = np.random.default_rng(3)
+    trajs = []
+    for k in range(30):
+        m = int(rng.integers(0, 50))
+        trajs.append(SimpleNamespace(
+            trajectory_id=k, prompt=SimpleNamespace(id=100 + k // 3),
+            tokens=[int(x) for x in rng.integers(0, 1000, size=m)],
+            behavior_logprobs=[float(x) for x in rng.normal(size=m)],
+            versions=[7] * m, reward=SimpleNamespace(reward=float(k % 2))))
+    ro, host = pack_trajectories(trajs)
+    torch.cuda.synchronize()
+    assert np.array_equal(ro.tokens.cpu().numpy(), np.concatenate([t.tokens for t in trajs]))
+    assert np.array_equal(ro.behav.cpu().numpy(),
+                          np.concatenate([t.behavior_logprobs for t in trajs]))
+    assert ro.versions is not None and int(ro.versions.sum()) == 7 * ro.n_tokens
+    assert ro.group_ids.cpu().tolist() == [k // 3 for k in range(30)]
+    assert ro.traj_bounds_host[-1] == ro.n_tokens
