@@ -14,7 +14,7 @@ import torch  # noqa: F401  (load torch's CUDA runtime before the library)
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libareal_b200.so")
 # tuning builds (tools/variants.py) can be selected explicitly; default: the in-tree build
-LIB_PATH = os.environ.get("AREAL_B200_LIB", LIB_PATH)
+LIB_PATH = os.environ.get("AREAL_B200_LIB") or LIB_PATH
 
 ABI_VERSION = 1
 N_STATS = 8

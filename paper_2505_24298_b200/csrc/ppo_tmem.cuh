@@ -392,20 +392,24 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
         const float F = g * fast_exp2(cw[c * kConsumerWarps + warp] - lse_s);
         const float2 F2 = make_float2(F, F);
         uint4* dst = reinterpret_cast<uint4*>(drow + (size_t)c * kChunkBytes);
+        auto scale_store = [&](int j) {
+          float f[E];
+          EFmt<T>::V::unpack(make_uint4(wv[4 * j], wv[4 * j + 1], wv[4 * j + 2], wv[4 * j + 3]), f);
 #pragma unroll
-        for (int j = 0; j < kVecPerThread; ++j) {
-          const int vi = vec_index(warp, lane, j);
-          if (full || vi < nvec) {
-            float f[E];
-            EFmt<T>::V::unpack(make_uint4(wv[4 * j], wv[4 * j + 1], wv[4 * j + 2], wv[4 * j + 3]), f);
-#pragma unroll
-            for (int e = 0; e < E; e += 2) {
-              const float2 d = fmul2(make_float2(f[e], f[e + 1]), F2);
-              f[e] = d.x;
-              f[e + 1] = d.y;
-            }
-            dst[vi] = Vec<T>::pack(f);
+          for (int e = 0; e < E; e += 2) {
+            const float2 d = fmul2(make_float2(f[e], f[e + 1]), F2);
+            f[e] = d.x;
+            f[e + 1] = d.y;
           }
+          dst[vec_index(warp, lane, j)] = Vec<T>::pack(f);
+        };
+        if (full) {  // branch-free
+#pragma unroll
+          for (int j = 0; j < kVecPerThread; ++j) scale_store(j);
+        } else {
+#pragma unroll
+          for (int j = 0; j < kVecPerThread; ++j)
+            if (vec_index(warp, lane, j) < nvec) scale_store(j);
         }
         c2.next(nslots);
       }
