@@ -24,6 +24,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -50,6 +51,7 @@ struct Args {
   float4* partials;  // [n_rows, n_vb]
   int64_t n_rows, vocab;
   int32_t dim, n_mt, n_vb, n_units;
+  int32_t group;  // vocab blocks interleaved per token tile (L2 working-set shaping)
   uint32_t idesc;
 };
 
@@ -122,6 +124,17 @@ __device__ __forceinline__ void tmem_ld32_issue(uint32_t taddr, float (&v)[32]) 
       : "memory");
 }
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// Unit u -> (token tile, vocab block).  `group` consecutive units share a token tile
+// and take `group` different vocab blocks, so the ~74 units in flight touch
+// 74/group H tiles and `group` W blocks: the L2 working set is
+// (74/group)*TM*d*2 + group*VB*d*2 bytes instead of 74*TM*d*2 (which exceeds L2
+// at d = 3584).  Units whose block lies past the vocab are empty.
+struct UnitXY { int mt, vb; };
+__device__ __forceinline__ UnitXY unit_xy(const Args& a, int u) {
+  const int g = u % a.group, r = u / a.group;
+  return UnitXY{r % a.n_mt, (r / a.n_mt) * a.group + g};
+}
 
 template <int STAGES_>
 struct Pipe {
@@ -225,7 +238,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (lane == 0) {
       Pipe<G::NSTAGE> p;
       for (int u = unit0; u < a.n_units; u += nunit_step) {
-        const int mt = u % a.n_mt, vb = u / a.n_mt;
+        const UnitXY xy = unit_xy(a, u);
+        const int mt = xy.mt, vb = xy.vb;
         const int32_t arow = mt * G::TM + (int32_t)rank * BM;
         for (int n = 0; n < NT; ++n) {
           const int64_t n0 = (int64_t)vb * VB + (int64_t)n * BN;
@@ -255,7 +269,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       Pipe<G::NSTAGE> p;
       uint32_t acc = 0, acc_phase = 0;
       for (int u = unit0; u < a.n_units; u += nunit_step) {
-        const int vb = u / a.n_mt;
+        const int vb = unit_xy(a, u).vb;
         for (int n = 0; n < NT; ++n) {
           const int64_t n0 = (int64_t)vb * VB + (int64_t)n * BN;
           if (n0 >= a.vocab) break;
@@ -305,7 +319,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint32_t acc = 0, acc_phase = 0, bpar = 0;
     constexpr float L2E = 1.4426950408889634f;
     // iteration order of (unit, N-tile) pairs, identical to the producer / MMA loops
-    auto tile_n0 = [&](int u, int n) -> int64_t { return (int64_t)(u / a.n_mt) * VB + (int64_t)n * BN; };
+    auto tile_n0 = [&](int u, int n) -> int64_t { return (int64_t)unit_xy(a, u).vb * VB + (int64_t)n * BN; };
     auto load_bias = [&](int64_t n0) -> float2 {
       float2 b2 = make_float2(0.f, 0.f);
       if (a.bias != nullptr && n0 >= 0) {
@@ -320,7 +334,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     named_bar_sync(1, EPI_THREADS);
     for (int u = unit0; u < a.n_units; u += nunit_step) {
-      const int mt = u % a.n_mt, vb = u / a.n_mt;
+      const UnitXY xy = unit_xy(a, u);
+      const int mt = xy.mt, vb = xy.vb;
       const int64_t row = (int64_t)mt * G::TM + (int64_t)rank * BM + r_local;
       int64_t tok = -1;
       if (row < a.n_rows) {
@@ -414,7 +429,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         bpar ^= 1u;
         named_bar_sync(1, EPI_THREADS);
       }
-      if (row < a.n_rows) a.partials[(row * a.n_vb + vb) * EPI_SPLIT + half] = make_float4(m, s, sx, xa);
+      if (row < a.n_rows && vb < a.n_vb)
+        a.partials[(row * a.n_vb + vb) * EPI_SPLIT + half] = make_float4(m, s, sx, xa);
     }
   }
   __syncthreads();
@@ -533,7 +549,20 @@ extern "C" int areal_linear_logprob_fwd(const void* hidden, int64_t ld_hidden, c
   const int cg = (cta_group == 1 || cta_group == 2) ? cta_group : (n_rows > BM ? 2 : 1);
   const int tm = BM * cg;
   a.n_mt = (int32_t)((n_rows + tm - 1) / tm);
-  a.n_units = a.n_mt * a.n_vb;
+  {
+    // group: minimise the L2 working set of the units in flight (see unit_xy)
+    const double in_flight = cg == 2 ? sms / 2 : sms;
+    int best = 1;
+    double best_bytes = 1e300;
+    for (int gsz = 1; gsz <= 8; gsz *= 2) {
+      const double bytes = (in_flight / gsz) * tm * (double)dim * 2 + gsz * (double)VB * dim * 2;
+      if (bytes < best_bytes) best = gsz, best_bytes = bytes;
+    }
+    const char* env = getenv("AREAL_K7_GROUP");
+    if (env && atoi(env) >= 1) best = atoi(env);
+    a.group = std::min(best, (int)a.n_vb);
+  }
+  a.n_units = a.n_mt * ((a.n_vb + a.group - 1) / a.group) * a.group;
   a.idesc = (1u << 4) | (ab << 7) | (ab << 10) | ((uint32_t)(BN >> 3) << 17) |
             ((uint32_t)((BM * cg) >> 4) << 24);
   if (!make_map(&tmA, hidden, dt, n_rows, dim, ld_hidden, BM) ||

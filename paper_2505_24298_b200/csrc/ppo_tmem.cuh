@@ -28,6 +28,21 @@
 namespace areal {
 
 constexpr int kTmemChunks = 8;        // 8 x 32 KB = the whole 256 KB of TMEM
+#ifndef AREAL_K2_PACKED_BF16_MUL
+#define AREAL_K2_PACKED_BF16_MUL 1
+#endif
+constexpr bool kK2PackedBf16Mul = AREAL_K2_PACKED_BF16_MUL != 0;
+
+__device__ __forceinline__ __nv_bfloat162 bits_bf162(uint32_t u) {
+  __nv_bfloat162 r;
+  memcpy(&r, &u, 4);
+  return r;
+}
+__device__ __forceinline__ uint32_t bf162_bits(__nv_bfloat162 v) {
+  uint32_t u;
+  memcpy(&u, &v, 4);
+  return u;
+}
 constexpr int kTmemCols = 512;
 constexpr int kTmemMaxChunks = 14;    // kTmemChunks + (nslots - 1) with 7 slots
 
@@ -392,16 +407,30 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
         const float F = g * fast_exp2(cw[c * kConsumerWarps + warp] - lse_s);
         const float2 F2 = make_float2(F, F);
         uint4* dst = reinterpret_cast<uint4*>(drow + (size_t)c * kChunkBytes);
+        // bf16 logits: e is stored as bf16 pairs, so dlogit = e * F is one packed
+        // bf16x2 multiply per two logits (HMUL2.BF16; F rounded to bf16, <= 2^-8
+        // relative, inside the bf16 contract) instead of unpack + FMUL2 + repack.
+        constexpr bool kPackedMul = std::is_same<T, __nv_bfloat16>::value && kK2PackedBf16Mul;
+        const __nv_bfloat162 Fb = __float2bfloat162_rn(F);
         auto scale_store = [&](int j) {
-          float f[E];
-          EFmt<T>::V::unpack(make_uint4(wv[4 * j], wv[4 * j + 1], wv[4 * j + 2], wv[4 * j + 3]), f);
+          if constexpr (kPackedMul) {
+            uint4 o;
+            o.x = bf162_bits(__hmul2(bits_bf162(wv[4 * j + 0]), Fb));
+            o.y = bf162_bits(__hmul2(bits_bf162(wv[4 * j + 1]), Fb));
+            o.z = bf162_bits(__hmul2(bits_bf162(wv[4 * j + 2]), Fb));
+            o.w = bf162_bits(__hmul2(bits_bf162(wv[4 * j + 3]), Fb));
+            dst[vec_index(warp, lane, j)] = o;
+          } else {
+            float f[E];
+            EFmt<T>::V::unpack(make_uint4(wv[4 * j], wv[4 * j + 1], wv[4 * j + 2], wv[4 * j + 3]), f);
 #pragma unroll
-          for (int e = 0; e < E; e += 2) {
-            const float2 d = fmul2(make_float2(f[e], f[e + 1]), F2);
-            f[e] = d.x;
-            f[e + 1] = d.y;
+            for (int e = 0; e < E; e += 2) {
+              const float2 d = fmul2(make_float2(f[e], f[e + 1]), F2);
+              f[e] = d.x;
+              f[e + 1] = d.y;
+            }
+            dst[vec_index(warp, lane, j)] = Vec<T>::pack(f);
           }
-          dst[vec_index(warp, lane, j)] = Vec<T>::pack(f);
         };
         if (full) {  // branch-free
 #pragma unroll

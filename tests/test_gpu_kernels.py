@@ -372,3 +372,45 @@ def test_packing_plan_matches_train_step_order():
         pt = plan.packed_traj.cpu().numpy()
         assert seq_cu[-1] == bounds[-1]
         assert np.array_equal(np.diff(seq_cu), np.diff(bounds)[pt])
+
+
+# ---------------------------------------------------------------- full-size properties
+def test_full_size_cfg2_microbatch_properties():
+    """BASELINE configs[1] at full size: one 32,768-token micro-batch of V=151,936 bf16
+    logits (10 GB) through K1 and K2 (in place), checked by size-independent
+    properties: K2's lp equals K1's; every dlogits row sums to ~0 (softmax - onehot)
+    and its token entry is g*(p_tok - 1); sampled rows equal a float64 torch
+    log-softmax restatement of trainer.py:163-182; counters add up; bit-identical
+    on a re-run (deterministic)."""
+    T, V = 32768, 151936
+    g = torch.Generator(device="cuda").manual_seed(0)
+    x = torch.empty(T, V, dtype=torch.bfloat16, device="cuda").normal_(0, 2, generator=g)
+    tok = torch.randint(0, V, (T,), device="cuda", generator=g)
+    lp1, _ = K.logprob_fwd(x, tok, with_entropy=False)
+    prox = lp1 + 0.02 * torch.randn(T, dtype=torch.float64, device="cuda", generator=g)
+    behav = prox + 0.1 * torch.randn(T, dtype=torch.float64, device="cuda", generator=g)
+    adv = torch.randn(T, dtype=torch.float64, device="cuda", generator=g)
+    sample = torch.randint(0, T, (48,), device="cuda", generator=g)
+    xs = x[sample].double()  # keep the sampled rows before the in-place backward
+    lp2 = torch.empty_like(lp1)
+    dl, st = K.ppo_fwd_bwd(x, tok, behav, prox, adv, dlogits=x, lp_out=lp2)  # in place
+    torch.testing.assert_close(lp2, lp1, rtol=0, atol=2e-5)
+    s = st.cpu().numpy()
+    assert s[1] + s[4] == T and s[7] == T
+    # the float64 restatement on the sampled rows
+    ref = O.surrogate_terms(xs.cpu().numpy(), tok[sample].cpu().numpy(),
+                            behav[sample].cpu().numpy(), prox[sample].cpu().numpy(),
+                            adv[sample].cpu().numpy())
+    got = dl[sample].double().cpu().numpy()
+    assert np.allclose(got, ref["dlogits"], rtol=2e-2, atol=2e-2 * np.abs(ref["dlogits"]).max(axis=1,
+                       keepdims=True) + 1e-30)
+    # row sums of (softmax - onehot) vanish; the token entry carries -g(1 - p)
+    rows = dl.double().sum(dim=1)
+    gtok = dl.gather(1, tok[:, None]).double()[:, 0]
+    assert float((rows.abs() - 2e-2 * gtok.abs()).max()) <= 1e-6
+    # determinism: a second pass over regenerated logits is bit-identical
+    y = torch.empty(T, V, dtype=torch.bfloat16, device="cuda").normal_(
+        0, 2, generator=torch.Generator(device="cuda").manual_seed(0))
+    dl2, st2 = K.ppo_fwd_bwd(y, tok, behav, prox, adv, dlogits=y)
+    assert torch.equal(dl2, dl) and torch.equal(st2, st)
+    del x, y
