@@ -110,6 +110,15 @@ __device__ __forceinline__ void load_values(const uint4* q, int warp, int lane, 
   }
 }
 
+// Diagnostic build knob (tools/variants.py): every K1 math thread arrives on the
+// slot's empty barrier itself, instead of lane 0 after __syncwarp.  Same ordering;
+// lets compute-sanitizer racecheck see the per-thread release (it does not model the
+// __syncwarp -> lane-0 arrive chain).
+#ifndef AREAL_K1_ARRIVE_ALL_LANES
+#define AREAL_K1_ARRIVE_ALL_LANES 0
+#endif
+constexpr bool kK1ArriveAllLanes = AREAL_K1_ARRIVE_ALL_LANES != 0;
+
 #ifndef AREAL_POLY_EVERY
 #define AREAL_POLY_EVERY 8
 #endif
@@ -234,7 +243,8 @@ __device__ __forceinline__ void row_ring_body(const PpoArgs& a) {
   if (tid == 0) {
     for (uint32_t s = 0; s < nslots; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kConsumerWarps);  // one arrive per math warp per use
+      // one arrive per math warp per use (K1 diagnostic build: one per math thread)
+      mbar_init(&empty[s], (!BWD && kK1ArriveAllLanes) ? kConsumerWarps * 32 : kConsumerWarps);
     }
     mbar_init(&tail->xbar[0], CS);
     mbar_init(&tail->xbar[1], CS);
@@ -376,8 +386,12 @@ __device__ __forceinline__ void row_ring_body(const PpoArgs& a) {
         A f[NV];
         load_values<T>(q, warp, lane, nvec, f);
         if (!BWD) {  // K1: the slot is free as soon as the values are in registers
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&empty[cc.slot]);
+          if (kK1ArriveAllLanes) {
+            mbar_arrive(&empty[cc.slot]);
+          } else {  // __syncwarp orders every lane's reads before lane 0's release-arrive
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[cc.slot]);
+          }
         }
         fold_values<T, ENT>(rs, f);
         cc.next(nslots);
