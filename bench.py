@@ -355,6 +355,7 @@ def run_ours(args, cfg):
     # ---------------- timed region: device-resident inputs
     runner.launches = 0
     runner.k1_events, runner.k2_events = [], []
+    runner.k3_events, runner.k45_events = [], []
     runner.k1_bytes = runner.k2_bytes = 0
     runner.record_events = True
     s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -374,6 +375,8 @@ def run_ours(args, cfg):
     launches = runner.launches  # all K steps of the timed region
     k2_ms = sum(s.elapsed_time(e) for s, e in runner.k2_events)
     k1_ms = sum(s.elapsed_time(e) for s, e in runner.k1_events)
+    k3_ms = sum(s.elapsed_time(e) for s, e in runner.k3_events)
+    k45_ms = sum(s.elapsed_time(e) for s, e in runner.k45_events)
     k2_bytes, k1_bytes = runner.k2_bytes, runner.k1_bytes
     n_k2 = len(runner.k2_events)
 
@@ -441,6 +444,12 @@ def run_ours(args, cfg):
             k1=dict(kernel="areal_logprob_fwd (K1)", achieved_gbs=k1_gbs, frac=k1_gbs / peak,
                     bytes_per_token=V * es + 16, ms_per_step=k1_ms / args.steps),
             k2=dict(ms_per_step=k2_ms / args.steps, tokens_per_s=T / (k2_ms / args.steps * 1e-3)),
+            k3=dict(kernel="areal_advantages (K3)", us_per_step=1e3 * k3_ms / args.steps,
+                    mode=hp.adv_mode, norm=hp.adv_norm),
+            k4_k5=dict(kernel="areal_plan_microbatches + areal_fill_gather (K4/K5)",
+                       us_per_step=1e3 * k45_ms / args.steps,
+                       note="all minibatches' allocation + packing plan, including the one "
+                            "small device->host read of the plan that sizes the model calls"),
             e2e=dict(value=T / (e2e_ms * 1e-3), unit="tokens/s", h2d_bytes_per_step=h2d,
                      d2h_bytes_per_step=d2h,
                      note="public API DecoupledPPOStep.run from pinned host rollouts; "

@@ -237,6 +237,8 @@ class DecoupledPPOStep:
         self.launches = 0  # kernels launched by this object (K1-K5)
         self.k1_events: list = []
         self.k2_events: list = []
+        self.k3_events: list = []   # advantages
+        self.k45_events: list = []  # allocation + packing plan (incl. its one host read)
         self.k2_bytes = 0
         self.k1_bytes = 0
         self.k7_flops = 0
@@ -320,8 +322,8 @@ class DecoupledPPOStep:
     def run(self, ro: PackedRollouts, logits_fn, backward_fn=None, update_fn=None,
             current_version: int = 0, dlogits_fn=None, prox_head_fn=None) -> StepResult:
         c = self.cfg
-        adv = self.advantages(ro)                               # trainer.py:296
-        sp = self.plan(ro)                                      # 300-315
+        adv = self._timed(self.k3_events, lambda: self.advantages(ro))  # trainer.py:296
+        sp = self._timed(self.k45_events, lambda: self.plan(ro))        # 300-315
         prox = self.prox_logprobs(ro, sp, logits_fn, prox_head_fn)  # 295 (before any update)
         decoupled = c.objective == "decoupled"
         M = len(sp.items)
