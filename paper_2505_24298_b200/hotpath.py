@@ -376,3 +376,65 @@ def emission_logprobs(tokens: torch.Tensor, logits: torch.Tensor | None = None,
         raise ValueError("hidden needs the LM-head weight")
     lp, _ = K.linear_logprob_fwd(hidden, weight, tokens, bias=bias)
     return lp
+
+
+def linear_ppo_fwd_bwd(hidden: torch.Tensor, weight: torch.Tensor, tokens: torch.Tensor,
+                       behav: torch.Tensor, prox: torch.Tensor, adv: torch.Tensor, *,
+                       bias: torch.Tensor | None = None, row_index: torch.Tensor | None = None,
+                       clip_eps: float = 0.2, decoupled: bool = True, versions=None,
+                       current_version: int = 0, eta_mask: int = -1,
+                       behav_weight_cap: float = 0.0, grad_scale: float = 1.0,
+                       chunk_tokens: int = 8192, stats: torch.Tensor | None = None,
+                       grad_weight: torch.Tensor | None = None,
+                       grad_bias: torch.Tensor | None = None, algo: str = "auto"):
+    """Decoupled-PPO loss + backward THROUGH the LM head, without materialising the
+    micro-batch's [T, V] logits: the rows are processed in chunks of ``chunk_tokens``.
+
+    _surrogate_terms (trainer.py:150-195) including its model GEMMs: per chunk,
+    logits = h W^T + b (cuBLAS bf16, fp32 accumulate) -> K2 in place -> dlogits,
+    then dH = dl W (trainer.py:183's residual^T features, transposed) and
+    dW += dl^T h, db += sum(dl) (trainer.py:183-184) accumulated in fp32.
+    Peak extra memory is chunk_tokens x V x 2 bytes (2.5 GB at 8,192 x 151,936)
+    instead of the full micro-batch's 10 GB.  Fusing the GEMMs into K2 does not pay
+    (DESIGN.md §8): a fused backward must recompute the logits GEMM.
+
+    Returns (grad_hidden [T, d] in hidden's dtype, grad_weight [V, d] fp32,
+    grad_bias [V] fp32 or None, stats float64[8]); all gradients are of
+    grad_scale * (-sum objective), like K2's dlogits.
+    """
+    if hidden.dim() != 2 or weight.dim() != 2 or hidden.shape[1] != weight.shape[1]:
+        raise ValueError("hidden [T, d] and weight [V, d] must share d")
+    if hidden.dtype != weight.dtype or hidden.dtype not in (torch.bfloat16, torch.float16):
+        raise TypeError("hidden and weight must both be bfloat16 or float16")
+    dev = hidden.device
+    T, d = hidden.shape
+    V = weight.shape[0]
+    if stats is None:
+        stats = torch.zeros(K._lib.N_STATS, dtype=torch.float64, device=dev)
+    if grad_weight is None:
+        grad_weight = torch.zeros(V, d, dtype=torch.float32, device=dev)
+    if bias is not None and grad_bias is None:
+        grad_bias = torch.zeros(V, dtype=torch.float32, device=dev)
+    grad_hidden = torch.empty_like(hidden)
+    bias16 = bias.to(hidden.dtype) if bias is not None else None
+    chunk = max(1, int(chunk_tokens))
+    buf = torch.empty((min(chunk, max(T, 1)), V), dtype=hidden.dtype, device=dev)
+    for lo in range(0, T, chunk):
+        hi = min(T, lo + chunk)
+        h = hidden[lo:hi]
+        lg = buf[: hi - lo]
+        if bias16 is not None:
+            torch.addmm(bias16, h, weight.t(), out=lg)
+        else:
+            torch.mm(h, weight.t(), out=lg)
+        ri = row_index[lo:hi] if row_index is not None else \
+            torch.arange(lo, hi, dtype=torch.int32, device=dev)
+        K.ppo_fwd_bwd(lg, tokens, behav, prox, adv, clip_eps=clip_eps, decoupled=decoupled,
+                      versions=versions, current_version=current_version, eta_mask=eta_mask,
+                      behav_weight_cap=behav_weight_cap, grad_scale=grad_scale, row_index=ri,
+                      dlogits=lg, stats=stats, algo=algo)
+        torch.mm(lg, weight, out=grad_hidden[lo:hi])                      # dH = dl W
+        grad_weight.add_(torch.mm(lg.t(), h, out_dtype=torch.float32))   # dW += dl^T h
+        if grad_bias is not None:
+            grad_bias.add_(lg.sum(dim=0, dtype=torch.float32))           # db += sum dl
+    return grad_hidden, grad_weight, grad_bias, stats

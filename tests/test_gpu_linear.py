@@ -90,3 +90,50 @@ def test_linear_logprob_rejects_bad_shapes():
         K.linear_logprob_fwd(h, w, t)  # d % 64 != 0
     with pytest.raises(TypeError):
         K.linear_logprob_fwd(h.float(), w.float(), t)
+
+
+@pytest.mark.parametrize("chunk", [64, 1000])
+def test_linear_ppo_fwd_bwd_matches_float64_autograd(chunk):
+    """Loss + backward through the LM head in token chunks (hotpath.linear_ppo_fwd_bwd)
+    vs float64 autograd of the restated objective (trainer.py:150-184) on the same
+    16-bit inputs: gradients wrt hidden, W and b, and the statistics."""
+    from paper_2505_24298_b200.hotpath import linear_ppo_fwd_bwd
+    T, V, d = 300, 5000, 128
+    h, w, b, tok = _case(T, V, d, seed=11)
+    g = torch.Generator(device=DEV).manual_seed(12)
+    x64 = h.double() @ w.double().t() + b.double()
+    lp = torch.log_softmax(x64, 1).gather(1, tok[:, None])[:, 0]
+    # ratios stay well inside (1-eps, 1+eps): the bf16 rounding of the head's logits
+    # (any bf16 LM head does it) must not flip a token across the clip boundary
+    prox = lp + 0.01 * torch.randn(T, dtype=torch.float64, device=DEV, generator=g)
+    behav = prox + 0.2 * torch.randn(T, dtype=torch.float64, device=DEV, generator=g)
+    adv = torch.randn(T, dtype=torch.float64, device=DEV, generator=g)
+    dh, dw, db, st = linear_ppo_fwd_bwd(h, w, tok, behav, prox, adv, bias=b, chunk_tokens=chunk)
+    # float64 autograd of -sum(objective), objective as trainer.py:165-176
+    H = h.double().requires_grad_(True)
+    W = w.double().requires_grad_(True)
+    B = b.double().requires_grad_(True)
+    lpa = torch.log_softmax(H @ W.t() + B, 1).gather(1, tok[:, None])[:, 0]
+    scale = torch.exp(prox - behav)
+    ratio = torch.exp(lpa - prox)
+    obj = scale * torch.minimum(ratio * adv, torch.clamp(ratio, 0.8, 1.2) * adv)
+    (-obj.sum()).backward()
+    # (1) tight: the float64 chain rule through the head's own bf16 logits (the same
+    # cuBLAS call), i.e. the restated _surrogate_terms on exactly what K2 sees
+    lg16 = torch.addmm(b.to(torch.bfloat16), h, w.t())
+    ref = O.surrogate_terms(lg16.double().cpu().numpy(), tok.cpu().numpy(), behav.cpu().numpy(),
+                            prox.cpu().numpy(), adv.cpu().numpy())
+    dl = torch.as_tensor(ref["dlogits"], device=DEV)
+    for got, r in ((dh, dl @ w.double()), (dw, dl.t() @ h.double()), (db, dl.sum(0))):
+        err = (got.double() - r).abs().max() / r.abs().max()
+        assert float(err) < 2e-2, float(err)
+    # (2) loose: float64 autograd with unrounded logits.  bf16 logits of magnitude ~16
+    # carry 0.06 absolute rounding (6% on individual probabilities): inherent in a bf16
+    # head, so this only guards signs and scales
+    for got, r in ((dh.double(), H.grad), (dw.double(), W.grad), (db.double(), B.grad)):
+        err = (got - r).abs().max() / r.abs().max()
+        assert float(err) < 1e-1, float(err)
+    s = st.cpu().numpy()
+    assert s[7] == T and s[1] == T and s[2] == 0
+    o = float(obj.detach().sum())
+    assert abs(s[0] - o) <= 2e-2 * max(1.0, abs(o))

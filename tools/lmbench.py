@@ -36,9 +36,23 @@ def timeit(fn):
     return s.elapsed_time(e) / a.iters
 
 
+behav = torch.full((T,), -12.0, dtype=torch.float64, device=dev)
+prox = behav + 0.01
+adv = torch.randn(T, dtype=torch.float64, device=dev)
+
 for which in a.which.split(","):
     if which == "fused":
         ms = timeit(lambda: K.linear_logprob_fwd(h, w, tok, bias=b, lp_out=lp, cta_group=a.cg))
+    elif which.startswith("ppo"):  # loss + backward through the head, chunked (ppo<chunk>)
+        from paper_2505_24298_b200.hotpath import linear_ppo_fwd_bwd
+        chunk = int(which[3:] or 8192)
+        gw = torch.zeros(V, d, dtype=torch.float32, device=dev)
+        gb = torch.zeros(V, dtype=torch.float32, device=dev)
+        ms = timeit(lambda: linear_ppo_fwd_bwd(h, w, tok, behav, prox, adv, bias=b,
+                                               chunk_tokens=chunk, grad_weight=gw, grad_bias=gb))
+        out[which] = dict(ms=ms, tflops_3gemm=6 * T * V * d / ms / 1e9, tok_s=T / ms * 1e3,
+                          peak_logits_gb=min(chunk, T) * V * 2 / 1e9)
+        continue
     elif which == "gemm":
         ms = timeit(lambda: torch.addmm(b.to(torch.bfloat16), h, w.t()))
     else:
