@@ -159,11 +159,19 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
 #endif
   return ok != 0;
 }
+// Slow-path back-off between polls (ns; 0 = none).  A failed try_wait wakes on every
+// transaction update of the barrier (a 32 KB bulk copy lands in pieces), so a
+// waiting warp would otherwise re-poll tens of times per chunk.
+#ifndef AREAL_WAIT_BACKOFF_NS
+#define AREAL_WAIT_BACKOFF_NS 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   if (mbar_try_wait(bar, parity)) return;
   const uint64_t t0 = globaltimer_ns();
-  while (!mbar_try_wait(bar, parity))
+  while (!mbar_try_wait(bar, parity)) {
+    if (AREAL_WAIT_BACKOFF_NS > 0) __nanosleep(AREAL_WAIT_BACKOFF_NS);
     if (globaltimer_ns() - t0 > kWaitLimitNs) __trap();
+  }
 }
 // acquire at cluster scope: pairs with remote release-arrives from peer CTAs.
 __device__ __forceinline__ bool mbar_try_wait_cluster(uint64_t* bar, uint32_t parity) {

@@ -28,6 +28,19 @@
 namespace areal {
 
 constexpr int kTmemChunks = 8;        // 8 x 32 KB = the whole 256 KB of TMEM
+// Warp max of a float through one REDUX.MAX on an order-preserving integer image
+// (one instruction instead of a 5-step shuffle/max chain on the per-chunk critical path).
+#ifndef AREAL_K2_REDUX_MAX
+#define AREAL_K2_REDUX_MAX 1
+#endif
+constexpr bool kRedux = AREAL_K2_REDUX_MAX != 0;
+__device__ __forceinline__ float warp_max_redux(float v) {
+  const int i = __float_as_int(v);
+  const int k = i ^ ((i >> 31) & 0x7fffffff);  // signed-int order == float order (no NaN)
+  const int m = __reduce_max_sync(0xffffffffu, k);
+  return __int_as_float(m ^ ((m >> 31) & 0x7fffffff));
+}
+
 #ifndef AREAL_K2_PACKED_BF16_MUL
 #define AREAL_K2_PACKED_BF16_MUL 1
 #endif
@@ -141,7 +154,7 @@ __device__ __forceinline__ float fold_to_e(RowStat<float>& rs, uint32_t (&w)[16]
   float lmax = f[0];
 #pragma unroll
   for (int i = 1; i < N; ++i) lmax = fmaxf(lmax, f[i]);
-  lmax = warp_max(lmax);
+  lmax = kRedux ? warp_max_redux(lmax) : warp_max(lmax);
   const float mn = fmaxf(rs.m, lmax);
   const float muse = (mn == Lim<float>::ninf()) ? 0.f : mn;
   const float c = Ex<float>::shift(muse);
