@@ -38,6 +38,7 @@ struct RingBcast {
   double lse;               // lse in shift units
   long long tok;            // token id
   unsigned long long dtok;  // dlogit of the token element (T bits)
+  int slow;                 // TMEM K2: statistics recomputed from HBM (fixed-shift overflow)
 };
 
 struct RingSmemTail {

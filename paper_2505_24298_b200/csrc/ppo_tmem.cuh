@@ -41,6 +41,17 @@ __device__ __forceinline__ float warp_max_redux(float v) {
   return __int_as_float(m ^ ((m >> 31) & 0x7fffffff));
 }
 
+// Fixed per-row shift: each warp takes its exp2 shift from the row's first chunk
+// (max via REDUX) and keeps it for the rest of the row, so later chunks need no max,
+// no warp reduction and no rescale.  A later logit more than ~88 above that shift
+// overflows e to inf; the epilogue sees a non-finite sum and recomputes the row's
+// statistics from HBM (still intact: pass 2 has not started), and pass 2 then
+// rebuilds dlogits from HBM too — a rare slow path, never a wrong result.
+#ifndef AREAL_K2_FIXED_SHIFT
+#define AREAL_K2_FIXED_SHIFT 1
+#endif
+constexpr bool kFixedShift = AREAL_K2_FIXED_SHIFT != 0;
+
 #ifndef AREAL_K2_PACKED_BF16_MUL
 #define AREAL_K2_PACKED_BF16_MUL 1
 #endif
@@ -151,14 +162,19 @@ __device__ __forceinline__ float fold_to_e(RowStat<float>& rs, uint32_t (&w)[16]
 #pragma unroll
     for (int e = 0; e < E; ++e) f[j * E + e] = ok ? g[e] : Lim<float>::ninf();
   }
-  float lmax = f[0];
+  // rs.m is warp-uniform; it stays -inf until a chunk with a finite value was seen
+  const bool need_max = !kFixedShift || rs.m == Lim<float>::ninf();
+  float lmax = Lim<float>::ninf();
+  if (need_max) {
+    lmax = f[0];
 #pragma unroll
-  for (int i = 1; i < N; ++i) lmax = fmaxf(lmax, f[i]);
-  lmax = kRedux ? warp_max_redux(lmax) : warp_max(lmax);
+    for (int i = 1; i < N; ++i) lmax = fmaxf(lmax, f[i]);
+    lmax = kRedux ? warp_max_redux(lmax) : warp_max(lmax);
+  }
   const float mn = fmaxf(rs.m, lmax);
   const float muse = (mn == Lim<float>::ninf()) ? 0.f : mn;
   const float c = Ex<float>::shift(muse);
-  const float r = Ex<float>::e(rs.m, c);
+  const float r = need_max ? Ex<float>::e(rs.m, c) : 1.f;
   const float2 L2 = make_float2(Lim<float>::kLog2e, Lim<float>::kLog2e);
   const float2 C2 = make_float2(-c, -c);
   float2 s2 = make_float2(0.f, 0.f), x2 = make_float2(0.f, 0.f);
@@ -201,6 +217,40 @@ __device__ __forceinline__ float chunk_to_e(RowStat<float>& rs, const uint4* q, 
   }
   lds_raw<false>(q, warp, lane, nvec, wv);
   return fold_to_e<T, ENT, false>(rs, wv, warp, lane, nvec);
+}
+
+// Exact (max, sum 2^x, sum 2^x * x) of a whole row straight from HBM, one warp,
+// 16-byte loads, two passes (the fixed-shift slow path; rows are 16-byte aligned).
+template <typename T, bool ENT>
+__device__ __noinline__ RowStat<float> row_stats_global(const PpoArgs& a, int64_t row, int lane) {
+  constexpr int E = Vec<T>::N;
+  const uint4* q = reinterpret_cast<const uint4*>(a.logits + row * a.ld_in_bytes);
+  const int64_t nvec = a.vocab / E;  // TMEM path: vocab * sizeof(T) % 16 == 0
+  float m = Lim<float>::ninf();
+  for (int64_t i = lane; i < nvec; i += 32) {
+    float f[E];
+    Vec<T>::unpack(q[i], f);
+#pragma unroll
+    for (int e = 0; e < E; ++e) m = fmaxf(m, f[e]);
+  }
+  m = warp_max(m);
+  const float c = (m == Lim<float>::ninf()) ? 0.f : m * Lim<float>::kLog2e;
+  float s = 0.f, sx = 0.f;
+  for (int64_t i = lane; i < nvec; i += 32) {
+    float f[E];
+    Vec<T>::unpack(q[i], f);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const float ee = fast_exp2(fmaf(f[e], Lim<float>::kLog2e, -c));
+      s += ee;
+      if (ENT) sx = fmaf(ee, fmaxf(f[e], Lim<float>::lowest()), sx);
+    }
+  }
+  RowStat<float> r;
+  r.m = m;
+  r.s = warp_sum(s);
+  r.sx = ENT ? warp_sum(sx) : 0.f;
+  return r;
 }
 
 template <typename T, bool ENT>
@@ -293,7 +343,9 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
       } else {
         w.init();
       }
-      const RowStat<A> tot = warp_merge(w);
+      RowStat<A> tot = warp_merge(w);
+      const bool slow = kFixedShift && !(tot.s < INFINITY);  // overflow (or NaN logits)
+      if (slow) tot = row_stats_global<T, ENT>(a, row, lane);
       const A lse_s = Ex<A>::lse_shift(tot.m == Lim<A>::ninf() ? A(0) : tot.m, tot.s);
       const double lse = Ex<A>::lse_nat(lse_s);
       const double ent = ENT ? lse - (double)(tot.sx / tot.s) : 0.0;
@@ -316,6 +368,7 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
         b.lse = (double)lse_s;
         b.tok = tok;
         b.dtok = to_bits<T>(Traits<T>::from_acc((A)(gc * (e_p - 1.0))));
+        b.slow = slow ? 1 : 0;
         mbar_arrive(&tail->bcbar[par]);
         stats_add(tail->st, t, ent);
         if (a.lp_out) a.lp_out[idx] = lp;
@@ -402,6 +455,41 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
       // stored its vector (same-thread program order => the patch lands last).
       // g == 0 rows still multiply (0 * e): NaN/inf logits give NaN, like the
       // reference's coef * (onehot - softmax).
+      if (kFixedShift && b.slow) {
+        // slow path: dlogits = g 2^(x log2e - lse) rebuilt from the row in HBM (each
+        // thread reads exactly the vectors it then overwrites: in-place safe)
+        const uint4* xrow = reinterpret_cast<const uint4*>(a.logits + row * a.ld_in_bytes);
+        const float2 L2 = make_float2(Lim<float>::kLog2e, Lim<float>::kLog2e);
+        const float2 C2 = make_float2(-lse_s, -lse_s);
+        const float2 G2 = make_float2(g, g);
+        Cursor cs = cur;
+        for (int c = 0; c < nchunks; ++c) {
+          const int nvec = (c < nfull ? kChunkBytes : last_bytes) / 16;
+          if (c >= ntm) {  // resident tail chunk: release its ring slot as usual
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[cs.slot]);
+          }
+          const uint4* src = xrow + (size_t)c * (kChunkBytes / 16);
+          uint4* dst = reinterpret_cast<uint4*>(drow + (size_t)c * kChunkBytes);
+#pragma unroll
+          for (int j = 0; j < kVecPerThread; ++j) {
+            const int vi = vec_index(warp, lane, j);
+            if (vi < nvec) {
+              float f[E];
+              Vec<T>::unpack(src[vi], f);
+#pragma unroll
+              for (int e = 0; e < E; e += 2) {
+                const float2 t = ffma2(make_float2(f[e], f[e + 1]), L2, C2);
+                const float2 d = fmul2(make_float2(fast_exp2(t.x), fast_exp2(t.y)), G2);
+                f[e] = d.x;
+                f[e + 1] = d.y;
+              }
+              dst[vi] = Vec<T>::pack(f);
+            }
+          }
+          cs.next(nslots);
+        }
+      } else {
       Cursor c2 = cur;
       for (int c = 0; c < nchunks; ++c) {
         const bool full = c < nfull;
@@ -455,6 +543,7 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
         }
         c2.next(nslots);
       }
+      }  // fast path
       {  // the one-hot element: owner of vector vt of chunk ct
         const int64_t per_chunk = kChunkBytes / (int)sizeof(T);
         if (b.tok >= 0 && b.tok < a.vocab) {

@@ -414,3 +414,34 @@ def test_full_size_cfg2_microbatch_properties():
     dl2, st2 = K.ppo_fwd_bwd(y, tok, behav, prox, adv, dlogits=y)
     assert torch.equal(dl2, dl) and torch.equal(st2, st)
     del x, y
+
+
+def test_ppo_tmem_fixed_shift_overflow_rows():
+    """K2's TMEM path fixes each warp's exp2 shift at the row's first chunk; a row whose
+    later logits exceed that shift by > 88 overflows and must take the HBM slow path
+    with identical results (vs the float64 oracle).  Also a NaN row (reference: the
+    token is excluded and its gradient is NaN) and an all-equal row."""
+    T, V = 12, 151936
+    logits, x64, tokens, behav, prox, adv = make_case(T, V, "bf16", seed=77)
+    lg = logits.clone()
+    lg[1, :20000] = -60.0          # first chunks low ...
+    lg[1, 100000:100010] = 70.0    # ... a later spike 130 above the fixed shift
+    lg[3, 140000] = 120.0          # single huge logit in the last (resident) chunk
+    lg[5, :] = 1.5                 # all equal
+    x64 = lg.double().numpy()
+    lp = O.token_logprobs(x64, tokens)
+    prox = lp + 0.01
+    behav = prox + 0.05
+    lg[7, 5000] = float("nan")     # NaN row
+    x64 = lg.double().numpy()
+    ref = O.surrogate_terms(x64, tokens, behav, prox, adv)
+    dl, st = K.ppo_fwd_bwd(lg.cuda(), cuda(tokens), cuda(behav), cuda(prox), cuda(adv))
+    got = dl.double().cpu().numpy()
+    ok_rows = [r for r in range(T) if r != 7]
+    assert np.allclose(got[ok_rows], ref["dlogits"][ok_rows], rtol=2e-2,
+                       atol=1e-3 * np.abs(ref["dlogits"][ok_rows]).max())
+    assert np.isnan(got[7]).all()
+    s = st.cpu().numpy()
+    assert s[1] == ref["stats"][1] and s[4] == ref["stats"][4]
+    lp_k, _ = K.logprob_fwd(lg.cuda(), cuda(tokens), with_entropy=False)
+    assert np.allclose(np.delete(lp_k.cpu().numpy(), 7), np.delete(ref["lp"], 7), atol=2e-2)

@@ -137,3 +137,28 @@ def test_linear_ppo_fwd_bwd_matches_float64_autograd(chunk):
     assert s[7] == T and s[1] == T and s[2] == 0
     o = float(obj.detach().sum())
     assert abs(s[0] - o) <= 2e-2 * max(1.0, abs(o))
+
+
+@pytest.mark.parametrize("cg", [1, 2])
+def test_linear_logprob_edge_shapes(cg):
+    # tiny vocab (< one 256-column tile), one row, empty batch, out-of-range token
+    for n, V, d in ((1, 7, 64), (3, 255, 64), (5, 257, 128)):
+        h, w, b, tok = _case(n, V, d, seed=n)
+        lp, ent = K.linear_logprob_fwd(h, w, tok, bias=b, with_entropy=True, cta_group=cg)
+        rlp, rent = _ref(h, w, b, tok)
+        torch.testing.assert_close(lp, rlp, rtol=0, atol=ATOL)
+        torch.testing.assert_close(ent, rent, rtol=1e-5, atol=ATOL)
+    h, w, b, tok = _case(4, 300, 64, seed=9)
+    tok[1] = 300  # out of range: lp = NaN (K1's documented behaviour), others unaffected
+    lp, _ = K.linear_logprob_fwd(h, w, tok, bias=b, cta_group=cg)
+    assert torch.isnan(lp[1]) and torch.isfinite(lp[[0, 2, 3]]).all()
+    empty = torch.empty(0, 64, dtype=torch.bfloat16, device=DEV)
+    lp0, _ = K.linear_logprob_fwd(empty, w, torch.empty(0, dtype=torch.int64, device=DEV))
+    assert lp0.numel() == 0
+
+
+def test_linear_logprob_deterministic():
+    h, w, b, tok = _case(700, 40000, 256, seed=21)
+    a1, e1 = K.linear_logprob_fwd(h, w, tok, bias=b, with_entropy=True)
+    a2, e2 = K.linear_logprob_fwd(h, w, tok, bias=b, with_entropy=True)
+    assert torch.equal(a1, a2) and torch.equal(e1, e2)
