@@ -308,13 +308,16 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 }  // namespace areal
 
 namespace areal {
-// 2^x on the FMA pipe (FA4-style MUFU offload) for x <= ~0: x = n + f with n the
+// 2^x on the FMA pipe (FA4-style MUFU offload): x = n + f with n the
 // nearest integer (1.5*2^23 rounding trick), 2^f by a degree-3 fit on [-0.5, 0.5]
 // (max relative error 7.5e-5: only for 16-bit outputs), 2^n added to the exponent
 // bits with one IMAD.  Arguments below -126 are clamped (result ~1e-38, vs 0).
 __device__ __forceinline__ float2 exp2_poly3(float2 x) {
-  x.x = fmaxf(x.x, -126.f);
-  x.y = fmaxf(x.y, -126.f);
+  // clamp to [-126, 129]: from ~128.5 the exponent add overflows into inf/NaN bits, so an
+  // overflowing argument still yields a non-finite value (detected by the fixed-shift
+  // folds) instead of a wrapped finite one
+  x.x = fminf(fmaxf(x.x, -126.f), 129.f);
+  x.y = fminf(fmaxf(x.y, -126.f), 129.f);
   const float2 t = fadd2(x, make_float2(12582912.f, 12582912.f));
   const float2 n = fadd2(t, make_float2(-12582912.f, -12582912.f));
   const float2 f = ffma2(n, make_float2(-1.f, -1.f), x);

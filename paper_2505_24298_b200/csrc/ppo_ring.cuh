@@ -125,20 +125,68 @@ constexpr bool kK1ArriveAllLanes = AREAL_K1_ARRIVE_ALL_LANES != 0;
 #endif
 constexpr int kPolyEvery = AREAL_POLY_EVERY;  // 0 disables the MUFU offload
 
+// Exact (max, sum 2^x, sum 2^x * x) of the 16-byte vectors [v0, v1) of a row straight
+// from HBM, one warp, two passes: the slow path of the fixed-shift folds (K1 here,
+// K2 in ppo_tmem.cuh) when a logit overflowed the row's shift.
+template <typename T, bool ENT>
+__device__ __noinline__ RowStat<float> row_stats_global(const PpoArgs& a, int64_t row, int64_t v0,
+                                                        int64_t v1, int lane) {
+  constexpr int E = Vec<T>::N;
+  const uint4* q = reinterpret_cast<const uint4*>(a.logits + row * a.ld_in_bytes);
+  float m = Lim<float>::ninf();
+  for (int64_t i = v0 + lane; i < v1; i += 32) {
+    float f[E];
+    Vec<T>::unpack(q[i], f);
+#pragma unroll
+    for (int e = 0; e < E; ++e) m = fmaxf(m, f[e]);
+  }
+  m = warp_max(m);
+  const float c = (m == Lim<float>::ninf()) ? 0.f : m * Lim<float>::kLog2e;
+  float s = 0.f, sx = 0.f;
+  for (int64_t i = v0 + lane; i < v1; i += 32) {
+    float f[E];
+    Vec<T>::unpack(q[i], f);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const float ee = fast_exp2(fmaf(f[e], Lim<float>::kLog2e, -c));
+      s += ee;
+      if (ENT) sx = fmaf(ee, fmaxf(f[e], Lim<float>::lowest()), sx);
+    }
+  }
+  RowStat<float> r;
+  r.m = m;
+  r.s = warp_sum(s);
+  r.sx = ENT ? warp_sum(sx) : 0.f;
+  return r;
+}
+
+// K1 fixed shift: each thread takes its exp2 shift from its first chunk of the row
+// and keeps it (no per-chunk max / rescale afterwards); overflow (a later logit
+// > ~88 above the shift) shows up as a non-finite sum and the epilogue recomputes
+// the row's statistics from HBM (row_stats_global).
+#ifndef AREAL_K1_FIXED_SHIFT
+#define AREAL_K1_FIXED_SHIFT 1
+#endif
+constexpr bool kK1FixedShift = AREAL_K1_FIXED_SHIFT != 0;
+
 // Fold this thread's values of one chunk into its running (m, s, sx).
 // fp32: packed f32x2 FFMA2/FADD2 around the MUFU ex2; fp64: scalar libdevice exp.
-template <typename T, bool ENT>
+template <typename T, bool ENT, bool FIXED = false>
 __device__ __forceinline__ void fold_values(RowStat<typename Traits<T>::Acc>& rs,
                                             const typename Traits<T>::Acc* f) {
   using A = typename Traits<T>::Acc;
   constexpr int N = kVecPerThread * Vec<T>::N;
-  A lmax = f[0];
+  const bool need_max = !FIXED || rs.m == Lim<A>::ninf();
+  A lmax = Lim<A>::ninf();
+  if (need_max) {
+    lmax = f[0];
 #pragma unroll
-  for (int i = 1; i < N; ++i) lmax = fmax(lmax, f[i]);
+    for (int i = 1; i < N; ++i) lmax = fmax(lmax, f[i]);
+  }
   const A mn = fmax(rs.m, lmax);
   const A muse = (mn == Lim<A>::ninf()) ? A(0) : mn;
   const A c = Ex<A>::shift(muse);
-  const A r = Ex<A>::e(rs.m, c);  // rescale of the running sums (0 while m = -inf)
+  const A r = need_max ? Ex<A>::e(rs.m, c) : A(1);  // rescale of the running sums (0 while m = -inf)
   if constexpr (std::is_same<A, float>::value) {
     const float2 L2 = make_float2(Lim<float>::kLog2e, Lim<float>::kLog2e);
     const float2 C2 = make_float2(-c, -c);
@@ -227,6 +275,9 @@ __device__ __forceinline__ void row_ring_body(const PpoArgs& a) {
   uint64_t* empty = full + nslots;
   RingSmemTail* tail = reinterpret_cast<RingSmemTail*>(empty + nslots);
 
+  // K1 (fp32 accumulation) folds with a fixed per-thread shift; K2-ring keeps the
+  // running max (its rows may be split over a cluster; the TMEM K2 has its own)
+  constexpr bool kFold1Fixed = !BWD && kK1FixedShift && std::is_same<A, float>::value;
   const int CS = a.cluster_size;
   const uint32_t rank = CS > 1 ? cluster_ctarank() : 0u;
   const int64_t cid = CS > 1 ? (int64_t)cluster_id_x() : (int64_t)blockIdx.x;
@@ -309,6 +360,10 @@ __device__ __forceinline__ void row_ring_body(const PpoArgs& a) {
       }
       w = warp_merge(w);  // every lane holds the CTA total
       if (!BWD && lane == 0) mbar_arrive(&tail->bcbar[par]);  // K1: partials consumed
+      if constexpr (kFold1Fixed) {
+        if (!(w.s < INFINITY))  // fixed-shift overflow (or NaN): exact, from HBM
+          w = row_stats_global<T, ENT>(a, row, b16, e16, lane);
+      }
       RowStat<A> tot = w;
       if (CS > 1) {
         // DSMEM exchange: lane r writes this CTA's partial into rank r's slot
@@ -394,7 +449,7 @@ __device__ __forceinline__ void row_ring_body(const PpoArgs& a) {
             if (lane == 0) mbar_arrive(&empty[cc.slot]);
           }
         }
-        fold_values<T, ENT>(rs, f);
+        fold_values<T, ENT, kFold1Fixed>(rs, f);
         cc.next(nslots);
       }
       const Cursor after = cc;  // ring position of the next row's chunk 0
@@ -423,7 +478,7 @@ __device__ __forceinline__ void row_ring_body(const PpoArgs& a) {
           const uint4* q = reinterpret_cast<const uint4*>(ring + (size_t)lc.slot * kChunkBytes);
           A f[NV];
           load_values<T>(q, warp, lane, nvec, f);
-          fold_values<T, ENT>(nxt, f);
+          fold_values<T, ENT, kFold1Fixed>(nxt, f);
           lc.next(nslots);
         }
         carry = nxt;

@@ -219,40 +219,6 @@ __device__ __forceinline__ float chunk_to_e(RowStat<float>& rs, const uint4* q, 
   return fold_to_e<T, ENT, false>(rs, wv, warp, lane, nvec);
 }
 
-// Exact (max, sum 2^x, sum 2^x * x) of a whole row straight from HBM, one warp,
-// 16-byte loads, two passes (the fixed-shift slow path; rows are 16-byte aligned).
-template <typename T, bool ENT>
-__device__ __noinline__ RowStat<float> row_stats_global(const PpoArgs& a, int64_t row, int lane) {
-  constexpr int E = Vec<T>::N;
-  const uint4* q = reinterpret_cast<const uint4*>(a.logits + row * a.ld_in_bytes);
-  const int64_t nvec = a.vocab / E;  // TMEM path: vocab * sizeof(T) % 16 == 0
-  float m = Lim<float>::ninf();
-  for (int64_t i = lane; i < nvec; i += 32) {
-    float f[E];
-    Vec<T>::unpack(q[i], f);
-#pragma unroll
-    for (int e = 0; e < E; ++e) m = fmaxf(m, f[e]);
-  }
-  m = warp_max(m);
-  const float c = (m == Lim<float>::ninf()) ? 0.f : m * Lim<float>::kLog2e;
-  float s = 0.f, sx = 0.f;
-  for (int64_t i = lane; i < nvec; i += 32) {
-    float f[E];
-    Vec<T>::unpack(q[i], f);
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const float ee = fast_exp2(fmaf(f[e], Lim<float>::kLog2e, -c));
-      s += ee;
-      if (ENT) sx = fmaf(ee, fmaxf(f[e], Lim<float>::lowest()), sx);
-    }
-  }
-  RowStat<float> r;
-  r.m = m;
-  r.s = warp_sum(s);
-  r.sx = ENT ? warp_sum(sx) : 0.f;
-  return r;
-}
-
 template <typename T, bool ENT>
 __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
   static_assert(sizeof(T) == 2 || sizeof(T) == 4, "TMEM K2 path: 16/32-bit logits");
@@ -345,7 +311,7 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
       }
       RowStat<A> tot = warp_merge(w);
       const bool slow = kFixedShift && !(tot.s < INFINITY);  // overflow (or NaN logits)
-      if (slow) tot = row_stats_global<T, ENT>(a, row, lane);
+      if (slow) tot = row_stats_global<T, ENT>(a, row, 0, (a.vocab * (int64_t)sizeof(T)) / 16, lane);
       const A lse_s = Ex<A>::lse_shift(tot.m == Lim<A>::ninf() ? A(0) : tot.m, tot.s);
       const double lse = Ex<A>::lse_nat(lse_s);
       const double ent = ENT ? lse - (double)(tot.sx / tot.s) : 0.0;

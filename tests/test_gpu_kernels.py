@@ -445,3 +445,23 @@ def test_ppo_tmem_fixed_shift_overflow_rows():
     assert s[1] == ref["stats"][1] and s[4] == ref["stats"][4]
     lp_k, _ = K.logprob_fwd(lg.cuda(), cuda(tokens), with_entropy=False)
     assert np.allclose(np.delete(lp_k.cpu().numpy(), 7), np.delete(ref["lp"], 7), atol=2e-2)
+
+
+@pytest.mark.parametrize("dt,V", [("bf16", 151936), ("bf16", 32000), ("f32", 32000), ("f16", 65536)])
+def test_logprob_fixed_shift_overflow_rows(dt, V):
+    """K1 folds with a fixed per-thread shift (from its first chunk); rows whose later
+    logits exceed it by > 88 overflow and must be recomputed from HBM exactly."""
+    T = 8
+    logits, x64, tokens, behav, prox, adv = make_case(T, V, dt, seed=5)
+    lg = logits.clone()
+    lg[0, : V // 2] = -60.0
+    lg[0, V - 100:] = 60.0 if dt == "f16" else 70.0
+    lg[2, V - 5] = 120.0 if dt != "f16" else 60000.0
+    lg[4, :] = -3.0
+    x64 = lg.double().numpy()
+    ref = O.token_logprobs(x64, tokens)
+    ent_ref = O.token_entropy(x64)
+    lp, ent = K.logprob_fwd(lg.cuda(), cuda(tokens))
+    ok, err = rel_close(lp.cpu().numpy(), ref, TOL[dt])
+    assert ok, err
+    assert np.allclose(ent.cpu().numpy(), ent_ref, rtol=TOL[dt], atol=TOL[dt] * 10)
