@@ -93,6 +93,21 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(PlanArgs a, int npow
       const int64_t len = a.bounds[traj + 1] - a.bounds[traj];
       a.status[m] = len < 1 ? AREAL_ERR_LEN_NONPOSITIVE : AREAL_ERR_LEN_EXCEEDS_CAPACITY;
       a.n_groups[m] = 0;
+      // still leave a valid (identity-order) packing so a K5 launch queued behind this
+      // plan stays in bounds; the caller raises on the status before using it
+      const int64_t t0 = a.mb_token_start[m];
+      a.group_cu[off + m] = t0;
+      a.group_seq_cu[off + m] = off;
+      int64_t t = t0;
+      for (int i = 0; i < n; ++i) {
+        const int32_t tr = a.item_traj[off + i];
+        a.group_of[off + i] = 0;
+        a.slot_of[off + i] = i;
+        a.packed_traj[off + i] = tr;
+        a.seq_cu[off + i] = t;
+        t += a.bounds[tr + 1] - a.bounds[tr];
+      }
+      if (m == a.n_minibatches - 1) a.seq_cu[a.n_items] = t;
     }
     return;
   }
@@ -181,8 +196,8 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(PlanArgs a, int npow
 
 // K5b: one warp per packed sequence writes its token gather indices (coalesced).
 __global__ void fill_gather_kernel(const int64_t* bounds, const int32_t* packed_traj,
-                                   const int64_t* seq_cu, int32_t n_items, int32_t* gather,
-                                   int32_t* seq_id) {
+                                   const int64_t* seq_cu, int32_t n_items, int64_t n_packed,
+                                   int32_t* gather, int32_t* seq_id) {
   const int lane = threadIdx.x & 31;
   const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -191,6 +206,7 @@ __global__ void fill_gather_kernel(const int64_t* bounds, const int32_t* packed_
     const int64_t src = bounds[traj];
     const int64_t len = bounds[traj + 1] - src;
     const int64_t dst = seq_cu[p];
+    if (dst < 0 || dst + len > n_packed) continue;  // never write outside gather[]
     for (int64_t i = lane; i < len; i += 32) {
       gather[dst + i] = (int32_t)(src + i);
       if (seq_id) seq_id[dst + i] = (int32_t)p;
@@ -248,7 +264,7 @@ extern "C" int areal_fill_gather(const int64_t* traj_bounds, const int32_t* pack
   if (!traj_bounds || !packed_traj || !seq_cu || !gather) return AREAL_ERR_INVALID_ARGUMENT;
   const int64_t blocks = std::min<int64_t>(((int64_t)n_items * 32 + 255) / 256, 148 * 16);
   fill_gather_kernel<<<(unsigned)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      traj_bounds, packed_traj, seq_cu, n_items, gather, seq_id);
+      traj_bounds, packed_traj, seq_cu, n_items, n_packed_tokens, gather, seq_id);
   AREAL_CUDA_CHECK_LAUNCH();
   return AREAL_OK;
 }

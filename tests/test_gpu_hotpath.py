@@ -149,3 +149,20 @@ def test_pack_trajectories_to_device():
     assert ro.versions is not None and int(ro.versions.sum()) == 7 * ro.n_tokens
     assert ro.group_ids.cpu().tolist() == [k // 3 for k in range(30)]
     assert ro.traj_bounds_host[-1] == ro.n_tokens
+
+
+def test_failed_plan_keeps_packing_in_bounds():
+    """A minibatch whose plan fails (sequence > budget) must still leave K5 a valid
+    packing: poison the allocator's recycled memory, fail the plan, and check the
+    device is healthy afterwards (regression: K5 read uninitialised plan entries)."""
+    from paper_2505_24298_b200.trainer import BatchError
+    junk = torch.full((1 << 24,), -7, dtype=torch.int64, device="cuda")
+    del junk
+    bounds = np.array([0, 50, 5000, 5100, 5200], dtype=np.int64)
+    tokens = np.zeros(5200, dtype=np.int64)
+    ro = PackedRollouts.from_host(bounds, tokens, np.zeros(5200), np.array([1.0, -1, 1, -1]))
+    runner = DecoupledPPOStep(HotPathConfig(minibatches=2, micro_token_budget=1000))
+    with pytest.raises(BatchError, match="exceeds capacity"):
+        runner.plan(ro)
+    torch.cuda.synchronize()
+    assert float(torch.ones(4, device="cuda").sum()) == 4.0
