@@ -84,6 +84,12 @@ typedef struct {
   int32_t eta_mask;         /* >= 0: mask tokens with cur_version - version > eta */
   int32_t current_version;  /* policy version being optimised                    */
   int32_t algo;             /* areal_algo_t                                       */
+  int32_t prox_from_lp;     /* 1: prox := this kernel's own lp (prox may be NULL).
+                             * Valid for the first minibatch of a step, whose params
+                             * are the batch-arrival params prox is defined under
+                             * (trainer.py:295 vs 315-321): the prox pass and the
+                             * loss then share one read of the logits, and the
+                             * ratio exp(lp - prox) is exactly 1 as in the reference */
 } areal_ppo_params_t;
 
 typedef enum { AREAL_ADV_REFERENCE = 0, AREAL_ADV_GAE = 1 } areal_adv_mode_t;

@@ -97,6 +97,10 @@ def surrogate_terms(logits, tokens, behav, prox, adv, clip_eps=0.2, decoupled=Tr
     x = np.asarray(logits, dtype=np.float64)
     toks = np.asarray(tokens, dtype=np.int64)
     behav = np.asarray(behav, dtype=np.float64)
+    if prox is None:
+        # first minibatch of a step: prox was computed under the same params as the
+        # current forward (trainer.py:295 vs 315-321), i.e. prox == lp exactly
+        prox = log_softmax(x)[np.arange(len(toks)), toks]
     prox = np.asarray(prox, dtype=np.float64)
     adv = np.asarray(adv, dtype=np.float64)
     n = len(toks)

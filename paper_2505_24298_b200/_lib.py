@@ -46,7 +46,7 @@ class PpoParams(ctypes.Structure):
     """areal_ppo_params_t"""
     _fields_ = [("clip_eps", c_f64), ("behav_weight_cap", c_f64), ("grad_scale", c_f64),
                 ("decoupled", c_i32), ("eta_mask", c_i32), ("current_version", c_i32),
-                ("algo", c_i32)]
+                ("algo", c_i32), ("prox_from_lp", c_i32)]
 
 
 class AdvParams(ctypes.Structure):

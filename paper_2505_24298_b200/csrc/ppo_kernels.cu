@@ -42,6 +42,7 @@ struct PpoArgs {
   unsigned int* counter;   // workspace: ticket for the last-CTA reduction
   double clip_eps, behav_cap, grad_scale;
   int decoupled, eta_mask, cur_version;
+  int prox_from_lp;        // prox := lp (first minibatch of a step)
   // ring kernel geometry
   int cluster_size;
   int64_t slice16;         // 16-byte units per cluster rank
@@ -286,7 +287,8 @@ __device__ __forceinline__ void row_warp_body(const PpoArgs& a) {
       if (a.lp_out) a.lp_out[idx] = lp;
       if (a.ent_out) a.ent_out[idx] = ent;
       if (BWD) {
-        const TokenTerms t = ppo_token(lp, a.behav[idx], a.prox ? a.prox[idx] : 0.0, a.adv[idx],
+        const double prox = a.prox_from_lp ? lp : (a.prox ? a.prox[idx] : 0.0);
+        const TokenTerms t = ppo_token(lp, a.behav[idx], prox, a.adv[idx],
                                        a.versions ? a.versions[idx] : 0, a);
         stats_add(st, t, a.ent_out ? ent : 0.0);
         gc = a.grad_scale * t.coef;
@@ -587,7 +589,7 @@ extern "C" int areal_ppo_fwd_bwd(const void* logits, int64_t ld_logits, void* dl
   if (n_rows < 0 || vocab < 1 || ld_logits < vocab || ld_dlogits < vocab) return AREAL_ERR_BAD_SHAPE;
   if (n_rows == 0) return AREAL_OK;
   if (!logits || !dlogits || !tokens || !behav || !adv || !stats) return AREAL_ERR_INVALID_ARGUMENT;
-  if (params->decoupled && !prox) return AREAL_ERR_INVALID_ARGUMENT;
+  if (params->decoupled && !prox && !params->prox_from_lp) return AREAL_ERR_INVALID_ARGUMENT;
   if (params->eta_mask >= 0 && !versions) return AREAL_ERR_INVALID_ARGUMENT;
   if (!workspace || workspace_bytes < AREAL_WORKSPACE_BYTES) return AREAL_ERR_WORKSPACE;
   PpoArgs a = {};
@@ -614,5 +616,6 @@ extern "C" int areal_ppo_fwd_bwd(const void* logits, int64_t ld_logits, void* dl
   a.decoupled = params->decoupled;
   a.eta_mask = params->eta_mask;
   a.cur_version = params->current_version;
+  a.prox_from_lp = params->prox_from_lp ? 1 : 0;
   return dispatch<true>(a, dtype, params->algo, static_cast<cudaStream_t>(stream));
 }

@@ -392,6 +392,7 @@ __device__ __forceinline__ void row_ring_body(const PpoArgs& a) {
       if (BWD) {
         sc_behav = __shfl_sync(0xffffffffu, sc_behav, 0);
         sc_prox = __shfl_sync(0xffffffffu, sc_prox, 0);
+        if (a.prox_from_lp) sc_prox = lp;  // first minibatch: prox is this lp
         // the three fp64 exponentials of the epilogue, one per lane, in parallel:
         // lane 0 exp(prox - behav), lane 1 exp(lp - prox | lp - behav), lane 2 exp(lp)
         const double arg = lane == 0 ? __dsub_rn(sc_prox, sc_behav)

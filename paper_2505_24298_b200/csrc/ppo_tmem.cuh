@@ -319,6 +319,7 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
       const double lp = xa - lse;
       sc_behav = __shfl_sync(0xffffffffu, sc_behav, 0);
       sc_prox = __shfl_sync(0xffffffffu, sc_prox, 0);
+      if (a.prox_from_lp) sc_prox = lp;  // first minibatch: prox is this lp
       const double arg = lane == 0 ? __dsub_rn(sc_prox, sc_behav)
                          : lane == 1 ? (a.decoupled ? __dsub_rn(lp, sc_prox) : __dsub_rn(lp, sc_behav))
                                      : lp;

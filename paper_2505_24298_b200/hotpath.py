@@ -54,6 +54,10 @@ class HotPathConfig:
     adv_norm: str = "global"
     adv_eps: float = 0.0
     algo: str = "auto"
+    # minibatch 0 trains under the batch-arrival params that define prox (trainer.py:295,
+    # no update precedes it), so its prox log-probs ARE its current log-probs: K2
+    # computes them in the same read of the logits (and the model skips that prox forward)
+    fuse_first_prox: bool = True
 
     def __post_init__(self):
         if not (0 < self.clip_eps < 1):
@@ -296,11 +300,13 @@ class DecoupledPPOStep:
 
     # ---- K1 (or fused K7) over this rank's micro-batches (prox, once per global batch)
     def prox_logprobs(self, ro: PackedRollouts, sp: StepPlan, logits_fn=None,
-                      head_fn=None) -> torch.Tensor:
+                      head_fn=None, skip_minibatches=()) -> torch.Tensor:
         # zeros: under DP each token's prox is written by exactly one rank, so a SUM
         # all-reduce (if a caller needs the full vector) reconstructs it
         prox = torch.zeros(ro.n_tokens, dtype=torch.float64, device=self.device)
         for m, groups in enumerate(sp.mine):
+            if m in skip_minibatches:  # filled by K2 (prox_from_lp) instead
+                continue
             for g, lo, hi in groups:
                 rows = sp.gather[lo:hi]
                 if head_fn is not None:  # trainer.py:128-137 with the output layer fused in
@@ -324,9 +330,12 @@ class DecoupledPPOStep:
         c = self.cfg
         adv = self._timed(self.k3_events, lambda: self.advantages(ro))  # trainer.py:296
         sp = self._timed(self.k45_events, lambda: self.plan(ro))        # 300-315
-        prox = self.prox_logprobs(ro, sp, logits_fn, prox_head_fn)  # 295 (before any update)
         decoupled = c.objective == "decoupled"
         M = len(sp.items)
+        fuse0 = c.fuse_first_prox and decoupled and M > 0
+        prox = self.prox_logprobs(ro, sp, logits_fn, prox_head_fn,       # 295 (before any update)
+                                  skip_minibatches=(0,) if fuse0 else ())
+        self.last_prox = prox
         mstats = torch.zeros((max(M, 1), K._lib.N_STATS), dtype=torch.float64, device=self.device)
         micro_count = 0
         for m in range(M):
@@ -335,11 +344,13 @@ class DecoupledPPOStep:
                 rows = sp.gather[lo:hi]
                 logits = logits_fn("train", m, g, rows)
                 dl_buf = dlogits_fn(m, g, logits) if dlogits_fn else None
+                first = fuse0 and m == 0
                 dl, _ = self._timed(self.k2_events, lambda: K.ppo_fwd_bwd(
                     logits, ro.tokens, ro.behav, prox, adv, clip_eps=c.clip_eps,
                     decoupled=decoupled, versions=ro.versions, current_version=current_version,
                     eta_mask=c.eta_mask, behav_weight_cap=c.behav_weight_cap, row_index=rows,
-                    dlogits=dl_buf, stats=st, algo=c.algo))
+                    dlogits=dl_buf, stats=st, algo=c.algo, prox_from_lp=first,
+                    lp_out=prox if first else None))
                 self.k2_bytes += (hi - lo) * (2 * logits.shape[1] * logits.element_size() + 52)
                 self.launches += 1
                 if backward_fn is not None:

@@ -108,7 +108,7 @@ def logprob_fwd(logits: torch.Tensor, tokens: torch.Tensor, row_index: torch.Ten
 def ppo_fwd_bwd(logits, tokens, behav, prox, adv, *, clip_eps=0.2, decoupled=True,
                 versions=None, current_version=0, eta_mask=-1, behav_weight_cap=0.0,
                 grad_scale=1.0, row_index=None, dlogits=None, lp_out=None, entropy_out=None,
-                stats=None, algo="auto"):
+                stats=None, algo="auto", prox_from_lp=False):
     """Fused decoupled/naive PPO loss + backward (K2).
 
     Returns ``(dlogits, stats)``: dlogits = grad_scale * coef * (softmax - onehot)
@@ -116,6 +116,11 @@ def ppo_fwd_bwd(logits, tokens, behav, prox, adv, *, clip_eps=0.2, decoupled=Tru
     accumulated with += (order: ``STAT_NAMES``).  ``dlogits`` may be ``logits``
     itself (in-place backward).  Per-token arrays are float64 indexed by global
     token (see ``row_index``).  Replaces trainer._surrogate_terms.
+
+    ``prox_from_lp=True`` (first minibatch of a step, whose params are the ones prox
+    is defined under, trainer.py:295): prox := the lp this kernel computes (``prox``
+    may be None; pass ``lp_out`` = the prox vector to record it), so the prox pass
+    and the loss share one read of the logits.
     """
     lib = _lib.load()
     n, v, ld, dt = _logits_info(logits)
@@ -124,7 +129,7 @@ def ppo_fwd_bwd(logits, tokens, behav, prox, adv, *, clip_eps=0.2, decoupled=Tru
     _need(tokens, "tokens", torch.int64, dev)
     _need(behav, "behav", torch.float64, dev, n_glob)
     _need(adv, "adv", torch.float64, dev, n_glob)
-    if decoupled:
+    if decoupled and not prox_from_lp:
         _need(prox, "prox", torch.float64, dev, n_glob)
     if versions is not None:
         _need(versions, "versions", torch.int32, dev, n_glob)
@@ -144,10 +149,11 @@ def ppo_fwd_bwd(logits, tokens, behav, prox, adv, *, clip_eps=0.2, decoupled=Tru
         if t is not None:
             _need(t, name, torch.float64, dev, n_glob)
     p = PpoParams(float(clip_eps), float(behav_weight_cap), float(grad_scale), int(bool(decoupled)),
-                  int(eta_mask), int(current_version), _lib.ALGO_CODES[algo])
+                  int(eta_mask), int(current_version), _lib.ALGO_CODES[algo], int(bool(prox_from_lp)))
     ws = workspace(dev)
     check(lib.areal_ppo_fwd_bwd(_ptr(logits), ld, _ptr(dlogits), ld_out, dt, n, v, _ptr(tokens),
-                                _ptr(behav), _ptr(prox if decoupled else None), _ptr(adv),
+                                _ptr(behav), _ptr(prox if decoupled and not prox_from_lp else None),
+                                _ptr(adv),
                                 _ptr(versions), _ptr(row_index), ctypes.byref(p), _ptr(lp_out),
                                 _ptr(entropy_out), _ptr(stats), _ptr(ws), ws.numel(), _stream()),
           "areal_ppo_fwd_bwd")

@@ -166,3 +166,30 @@ def test_failed_plan_keeps_packing_in_bounds():
         runner.plan(ro)
     torch.cuda.synchronize()
     assert float(torch.ones(4, device="cuda").sum()) == 4.0
+
+
+def test_fused_first_prox_matches_unfused():
+    # fuse_first_prox (K2 computes minibatch 0's prox in its own read of the logits)
+    # == the unfused path (K1 prox pass over every micro-batch), same logits
+    bounds, T, V, table, x64, tokens, behav, rewards, versions = _setup(seed=5)
+    ro = PackedRollouts.from_host(bounds, tokens, behav, rewards, versions=versions)
+    dev_table = table.cuda()
+    outs = []
+    for fuse in (False, True):
+        calls = []
+
+        def logits_fn(phase, m, g, rows):
+            calls.append((phase, m))
+            return dev_table.index_select(0, rows.long())
+        cfg = HotPathConfig(minibatches=3, micro_token_budget=700, micro_min_groups=2,
+                            fuse_first_prox=fuse)
+        runner = DecoupledPPOStep(cfg)
+        res = runner.run(ro, logits_fn, current_version=10)
+        outs.append((res.minibatch_stats, runner.last_prox.cpu().numpy(), calls))
+    (s0, p0, c0), (s1, p1, c1) = outs
+    assert not any(ph == "prox" and m == 0 for ph, m in c1)   # no prox forward for minibatch 0
+    assert any(ph == "prox" and m == 0 for ph, m in c0)
+    counts = [1, 2, 4, 5, 7]
+    assert np.array_equal(s0[:, counts], s1[:, counts])
+    np.testing.assert_allclose(s1, s0, rtol=2e-2, atol=1e-6)
+    np.testing.assert_allclose(p1, p0, rtol=0, atol=2e-5)

@@ -465,3 +465,22 @@ def test_logprob_fixed_shift_overflow_rows(dt, V):
     ok, err = rel_close(lp.cpu().numpy(), ref, TOL[dt])
     assert ok, err
     assert np.allclose(ent.cpu().numpy(), ent_ref, rtol=TOL[dt], atol=TOL[dt] * 10)
+
+
+@pytest.mark.parametrize("dt,V,algo", [("bf16", 151936, "auto"), ("bf16", 32000, "ring"),
+                                       ("f32", 32000, "auto"), ("f64", 1000, "warp"),
+                                       ("bf16", 4096, "warp")])
+def test_ppo_prox_from_lp(dt, V, algo):
+    """prox_from_lp (first minibatch): prox := the kernel's own lp, written to lp_out;
+    equals the oracle with prox = lp (ratio exactly 1, trainer.py:295 vs 315-321)."""
+    T = 64
+    logits, x64, tokens, behav, prox, adv = make_case(T, V, dt, seed=41)
+    ref = O.surrogate_terms(x64, tokens, behav, None, adv)
+    lp = torch.zeros(T, dtype=torch.float64, device="cuda")
+    dl, st = K.ppo_fwd_bwd(logits.cuda(), cuda(tokens), cuda(behav), None, cuda(adv),
+                           prox_from_lp=True, lp_out=lp, algo=algo)
+    check_k2(dt, dl.double().cpu().numpy(), st.cpu().numpy(), ref, T)
+    ok, err = rel_close(lp.cpu().numpy(), ref["lp"], TOL[dt])
+    assert ok, err
+    s = st.cpu().numpy()
+    assert abs(s[3] - s[1]) <= 1e-9 * max(1.0, s[1])  # every valid ratio is exactly 1
