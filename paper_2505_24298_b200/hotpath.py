@@ -397,7 +397,8 @@ def linear_ppo_fwd_bwd(hidden: torch.Tensor, weight: torch.Tensor, tokens: torch
                        behav_weight_cap: float = 0.0, grad_scale: float = 1.0,
                        chunk_tokens: int = 8192, stats: torch.Tensor | None = None,
                        grad_weight: torch.Tensor | None = None,
-                       grad_bias: torch.Tensor | None = None, algo: str = "auto"):
+                       grad_bias: torch.Tensor | None = None, algo: str = "auto",
+                       prox_from_lp: bool = False, lp_out: torch.Tensor | None = None):
     """Decoupled-PPO loss + backward THROUGH the LM head, without materialising the
     micro-batch's [T, V] logits: the rows are processed in chunks of ``chunk_tokens``.
 
@@ -408,6 +409,8 @@ def linear_ppo_fwd_bwd(hidden: torch.Tensor, weight: torch.Tensor, tokens: torch
     Peak extra memory is chunk_tokens x V x 2 bytes (2.5 GB at 8,192 x 151,936)
     instead of the full micro-batch's 10 GB.  Fusing the GEMMs into K2 does not pay
     (DESIGN.md §8): a fused backward must recompute the logits GEMM.
+
+    ``prox_from_lp`` / ``lp_out``: as in kernels.ppo_fwd_bwd (first minibatch of a step).
 
     Returns (grad_hidden [T, d] in hidden's dtype, grad_weight [V, d] fp32,
     grad_bias [V] fp32 or None, stats float64[8]); all gradients are of
@@ -443,7 +446,8 @@ def linear_ppo_fwd_bwd(hidden: torch.Tensor, weight: torch.Tensor, tokens: torch
         K.ppo_fwd_bwd(lg, tokens, behav, prox, adv, clip_eps=clip_eps, decoupled=decoupled,
                       versions=versions, current_version=current_version, eta_mask=eta_mask,
                       behav_weight_cap=behav_weight_cap, grad_scale=grad_scale, row_index=ri,
-                      dlogits=lg, stats=stats, algo=algo)
+                      dlogits=lg, stats=stats, algo=algo, prox_from_lp=prox_from_lp,
+                      lp_out=lp_out)
         torch.mm(lg, weight, out=grad_hidden[lo:hi])                      # dH = dl W
         grad_weight.add_(torch.mm(lg.t(), h, out_dtype=torch.float32))   # dW += dl^T h
         if grad_bias is not None:
