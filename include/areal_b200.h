@@ -234,6 +234,11 @@ typedef struct {
   double bias_correction1, bias_correction2;             /* 1 - beta**step (policy.py:249-250) */
   double grad_scale;                                     /* -1/n (trainer.py:330) or 1 */
   int32_t exact_norm;                                    /* 1: numpy-exact fp64 norm */
+  /* optional DEVICE pointer: if set, the scale is grad_scale / max(*grad_scale_divisor, 1)
+   * computed on the device — e.g. grad_scale = -1 and the divisor = the all-reduced
+   * n_valid statistic of K2 (stats[1]), i.e. trainer.py:329-330's -1/max(n,1) with no
+   * host synchronisation between the loss and the optimizer step */
+  const double* grad_scale_divisor;
 } areal_adam_params_t;
 
 int areal_adam_step(const areal_adam_tensor_t* tensors, int32_t n_tensors, int param_dtype,

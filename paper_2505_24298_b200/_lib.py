@@ -66,7 +66,8 @@ class AdamParams(ctypes.Structure):
     _fields_ = [("lr", c_f64), ("beta1", c_f64), ("beta2", c_f64), ("eps", c_f64),
                 ("weight_decay", c_f64), ("clip_norm", c_f64), ("one_minus_beta1", c_f64),
                 ("one_minus_beta2", c_f64), ("bias_correction1", c_f64),
-                ("bias_correction2", c_f64), ("grad_scale", c_f64), ("exact_norm", c_i32)]
+                ("bias_correction2", c_f64), ("grad_scale", c_f64), ("exact_norm", c_i32),
+                ("grad_scale_divisor", c_vp)]
 
 
 ADAM_MAX_TENSORS = 32

@@ -43,6 +43,7 @@ struct AdamArgs {
   int32_t leaf_start[kAdamMaxTensors + 1];
   int32_t n_tensors;
   double lr, b1, b2, omb1, omb2, eps, wd, c1, c2, clip, gscale;
+  const double* gdiv;  // optional device divisor of gscale (K2's n_valid)
   double* ws;        // [0] norm, [1] factor, [2] non-finite count (as u64), [16..] partials
   double* norm_out;  // optional device [2]: norm, non-finite count
 };
@@ -61,6 +62,12 @@ template <> __device__ __forceinline__ void st_from_f64<__nv_bfloat16>(void* bas
 }
 template <> __device__ __forceinline__ void st_from_f64<__half>(void* base, int64_t i, double x) {
   static_cast<__half*>(base)[i] = __double2half(x);
+}
+
+// grad_scale, or grad_scale / max(n, 1) with n read on the device (the same IEEE
+// division Python's -1.0 / n performs at trainer.py:330)
+__device__ __forceinline__ double eff_scale(const AdamArgs& a) {
+  return a.gdiv ? __ddiv_rn(a.gscale, fmax(*a.gdiv, 1.0)) : a.gscale;
 }
 
 __device__ __forceinline__ int tensor_of(const AdamArgs& a, int64_t e) {
@@ -95,7 +102,7 @@ __global__ void __launch_bounds__(kAdamThreads) adam_sumsq_exact_kernel(const __
     while (k + 1 < a.n_tensors && a.leaf_start[k + 1] <= leaf) ++k;
     int64_t off, len;
     pw_node(a.n[k], a.depth[k], leaf - a.leaf_start[k], off, len);
-    a.ws[16 + leaf] = pw_sum_f(ScaledSq<G>{a.g[k], a.gscale, &bad}, off, len);
+    a.ws[16 + leaf] = pw_sum_f(ScaledSq<G>{a.g[k], eff_scale(a), &bad}, off, len);
   }
   bad = __reduce_add_sync(0xffffffffu, bad);
   if ((threadIdx.x & 31) == 0 && bad) atomicAdd(nonfinite_counter(a), (unsigned long long)bad);
@@ -108,11 +115,12 @@ __global__ void __launch_bounds__(kAdamThreads) adam_sumsq_fast_kernel(const __g
   double acc = 0.0;
   unsigned bad = 0;
   const int64_t total = a.start[a.n_tensors];
+  const double gscale = eff_scale(a);
   int k = 0;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     while (a.start[k + 1] <= e) ++k;
-    const double x = ld_as_f64<G>(a.g[k], e - a.start[k]) * a.gscale;
+    const double x = ld_as_f64<G>(a.g[k], e - a.start[k]) * gscale;
     if (!isfinite(x)) ++bad;
     acc = fma(x, x, acc);
   }
@@ -179,13 +187,14 @@ __global__ void __launch_bounds__(kAdamThreads) adam_update_kernel(const __grid_
   if (*nonfinite_counter(a) != 0ull) return;  // reference raises before touching state
   const double factor = a.ws[1];
   const bool clip = factor != 1.0;
+  const double gscale = eff_scale(a);
   const int64_t total = a.start[a.n_tensors];
   int k = 0;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     while (a.start[k + 1] <= e) ++k;
     const int64_t i = e - a.start[k];
-    double g = __dmul_rn(ld_as_f64<G>(a.g[k], i), a.gscale);
+    double g = __dmul_rn(ld_as_f64<G>(a.g[k], i), gscale);
     if (clip) g = __dmul_rn(g, factor);
     double m = ld_as_f64<P>(a.m[k], i), v = ld_as_f64<P>(a.v[k], i), p = ld_as_f64<P>(a.p[k], i);
     m = __dadd_rn(__dmul_rn(a.b1, m), __dmul_rn(a.omb1, g));
@@ -271,6 +280,7 @@ extern "C" int areal_adam_step(const areal_adam_tensor_t* tensors, int32_t n_ten
   a.c2 = params->bias_correction2;
   a.clip = params->clip_norm;
   a.gscale = params->grad_scale;
+  a.gdiv = params->grad_scale_divisor;
   // K6 shares the upper half of the workspace with K3 (stream-ordered); the lower
   // half holds K2's zeroed ticket counter and partials.
   a.ws = reinterpret_cast<double*>(static_cast<char*>(workspace) + AREAL_WORKSPACE_BYTES / 2);

@@ -266,7 +266,8 @@ def fill_gather(traj_bounds, plan: DevicePlan, n_packed_tokens: int, with_seq_id
 # ---------------------------------------------------------------- K6
 def adam_step(params, grads, exp_avgs, exp_avg_sqs, *, step: int, lr: float, beta1: float,
               beta2: float, eps: float, weight_decay: float, clip_norm: float,
-              grad_scale: float = 1.0, exact_norm: bool | None = None, norm_out=None):
+              grad_scale: float = 1.0, exact_norm: bool | None = None, norm_out=None,
+              grad_scale_divisor: torch.Tensor | None = None):
     """Fused global-norm clip + Adam over a list of tensors (K6), in place.
 
     Mirrors policy.apply_update (policy.py:225-258) applied to ``grad * grad_scale``
@@ -275,6 +276,9 @@ def adam_step(params, grads, exp_avgs, exp_avg_sqs, *, step: int, lr: float, bet
     tensor [global_norm, n_nonfinite]; when n_nonfinite > 0 nothing was updated and
     the caller raises NonFiniteGradientError.  ``exact_norm`` (default: fp64 params)
     replays numpy's pairwise sums so the update is bit-identical to the reference.
+    ``grad_scale_divisor`` (a 1-element float64 CUDA tensor, e.g. ``stats[1:2]`` of K2 after
+    the all-reduce) makes the scale ``grad_scale / max(divisor, 1)`` on the device, so
+    the loss -> optimizer hand-off needs no host synchronisation.
     """
     lib = _lib.load()
     n = len(params)
@@ -307,7 +311,10 @@ def adam_step(params, grads, exp_avgs, exp_avg_sqs, *, step: int, lr: float, bet
     # scalars exactly as the reference computes them in Python (policy.py:245-250)
     prm = _lib.AdamParams(float(lr), float(beta1), float(beta2), float(eps), float(weight_decay),
                           float(clip_norm), 1 - beta1, 1 - beta2, 1 - beta1 ** step,
-                          1 - beta2 ** step, float(grad_scale), int(bool(exact_norm)))
+                          1 - beta2 ** step, float(grad_scale), int(bool(exact_norm)),
+                          _ptr(grad_scale_divisor))
+    if grad_scale_divisor is not None:
+        _need(grad_scale_divisor, "grad_scale_divisor", torch.float64, dev, 1)
     if norm_out is None:
         norm_out = torch.empty(2, dtype=torch.float64, device=dev)
     _need(norm_out, "norm_out", torch.float64, dev, 2)

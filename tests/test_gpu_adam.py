@@ -121,3 +121,28 @@ def test_adam_rejects_bad_arguments():
     with pytest.raises(ValueError):
         K.adam_step([p], [p[:2]], [p], [p], step=1, lr=1, beta1=0.9, beta2=0.9, eps=1,
                     weight_decay=0, clip_norm=1)
+
+
+def test_adam_device_divisor_bit_identical():
+    """grad_scale = -1 with the divisor n on the device (K2's all-reduced n_valid) gives
+    the same bits as the host-computed -1.0/n (trainer.py:330), with no host sync."""
+    for c in load_cases("adam.npz")[:3]:
+        W = torch.as_tensor(c["W0"], device=DEV).clone()
+        b = torch.as_tensor(c["b0"], device=DEV).clone()
+        mw, vw, mb, vb = (torch.zeros_like(W), torch.zeros_like(W), torch.zeros_like(b),
+                          torch.zeros_like(b))
+        for k in range(int(c["steps"])):
+            n_dev = torch.tensor([float(int(c[f"n{k}"]))], dtype=torch.float64, device=DEV)
+            K.adam_step([W, b], [torch.as_tensor(c[f"gw{k}"], device=DEV),
+                                 torch.as_tensor(c[f"gb{k}"], device=DEV)], [mw, mb], [vw, vb],
+                        step=k + 1, lr=float(c["lr"]), beta1=0.9, beta2=0.95, eps=1e-5,
+                        weight_decay=float(c["wd"]), clip_norm=float(c["clip"]),
+                        grad_scale=-1.0, grad_scale_divisor=n_dev)
+        assert np.array_equal(W.cpu().numpy(), c["W"]) and np.array_equal(b.cpu().numpy(), c["b"])
+    # divisor 0 -> max(n, 1) = 1 (trainer.py:329)
+    p = torch.ones(5, device=DEV)
+    K.adam_step([p], [torch.ones(5, device=DEV)], [torch.zeros(5, device=DEV)],
+                [torch.zeros(5, device=DEV)], step=1, lr=0.1, beta1=0.9, beta2=0.95, eps=1e-8,
+                weight_decay=0.0, clip_norm=0.0, grad_scale=1.0,
+                grad_scale_divisor=torch.zeros(1, dtype=torch.float64, device=DEV))
+    torch.testing.assert_close(p, torch.full((5,), 0.9, device=DEV), rtol=1e-6, atol=1e-6)
