@@ -162,3 +162,32 @@ def test_linear_logprob_deterministic():
     a1, e1 = K.linear_logprob_fwd(h, w, tok, bias=b, with_entropy=True)
     a2, e2 = K.linear_logprob_fwd(h, w, tok, bias=b, with_entropy=True)
     assert torch.equal(a1, a2) and torch.equal(e1, e2)
+
+
+def test_linear_ppo_fwd_bwd_row_index_and_prox_from_lp():
+    """row_index (packed rows -> global tokens) and prox_from_lp (first minibatch):
+    chunked backward through the head == the unchunked call; prox written via lp_out."""
+    from paper_2505_24298_b200.hotpath import linear_ppo_fwd_bwd
+    T, V, d = 257, 3000, 64
+    h, w, b, tok_rows = _case(T, V, d, seed=31)
+    g = torch.Generator(device=DEV).manual_seed(32)
+    perm = torch.randperm(T, device=DEV, generator=g).to(torch.int32)
+    tokens = torch.empty(T, dtype=torch.int64, device=DEV)
+    tokens[perm.long()] = tok_rows
+    behav = torch.full((T,), -8.0, dtype=torch.float64, device=DEV)
+    adv = torch.randn(T, dtype=torch.float64, device=DEV, generator=g)
+    outs = []
+    for chunk in (50, T):
+        lp = torch.zeros(T, dtype=torch.float64, device=DEV)
+        dh, dw, db, st = linear_ppo_fwd_bwd(h, w, tokens, behav, None, adv, bias=b,
+                                            row_index=perm, chunk_tokens=chunk,
+                                            prox_from_lp=True, lp_out=lp)
+        outs.append((dh.float(), dw, db, st, lp))
+    for a, c in zip(outs[0], outs[1]):
+        torch.testing.assert_close(a, c, rtol=1e-4, atol=1e-5)
+    # prox == the float64 log-softmax of the head's own bf16 logits (what K2 reads)
+    lg16 = torch.addmm(b.to(torch.bfloat16), h, w.t()).double()
+    rlp = torch.log_softmax(lg16, 1).gather(1, tok_rows[:, None])[:, 0]
+    torch.testing.assert_close(outs[0][4][perm.long()], rlp, rtol=0, atol=1e-4)
+    s = outs[0][3].cpu().numpy()
+    assert s[1] == T and abs(s[3] - T) < 1e-9  # every ratio exactly 1
