@@ -48,6 +48,31 @@ def test_library_validates_without_gpu():
     assert rc == _lib.ERR_MIN_GROUPS
     # zero rows is a no-op
     assert lib.areal_logprob_fwd(None, 16, 0, 0, 16, None, None, None, None, 0, None, 0, None) == 0
+    # decoupled without prox is only legal with prox_from_lp (then the kernel would run)
+    p2 = _lib.PpoParams(0.2, 0.0, 1.0, 1, -1, 0, 0, 0)
+    rc = lib.areal_ppo_fwd_bwd(ctypes.c_void_p(16), 16, ctypes.c_void_p(16), 16, 0, 4, 16,
+                               ctypes.c_void_p(16), ctypes.c_void_p(16), None, ctypes.c_void_p(16),
+                               None, None, ctypes.byref(p2), None, None, ctypes.c_void_p(16),
+                               None, 0, None)
+    assert rc == _lib.ERR_INVALID_ARGUMENT
+    # K6: dtype / tensor-count validation
+    t = (_lib.AdamTensor * 1)()
+    ap = _lib.AdamParams(1e-3, 0.9, 0.95, 1e-8, 0.0, 1.0, 0.1, 0.05, 0.1, 0.05, 1.0, 1, None)
+    ws = ctypes.create_string_buffer(_lib.WORKSPACE_BYTES)
+    assert lib.areal_adam_step(t, 1, 0, 0, ctypes.byref(ap), None, ws, _lib.WORKSPACE_BYTES,
+                               None) == _lib.ERR_UNSUPPORTED  # exact norm needs fp64
+    assert lib.areal_adam_step(t, 33, 3, 3, ctypes.byref(ap), None, ws, _lib.WORKSPACE_BYTES,
+                               None) == _lib.ERR_INVALID_ARGUMENT
+    # K7: shape / alignment / dtype validation
+    assert lib.areal_linear_logprob_fwd(ctypes.c_void_p(256), 100, ctypes.c_void_p(256), 100,
+                                        None, 1, 4, 1000, 100, ctypes.c_void_p(256), None,
+                                        ctypes.c_void_p(256), None, None, 0, 0, None) \
+        == _lib.ERR_UNSUPPORTED  # dim % 64 != 0
+    assert lib.areal_linear_logprob_fwd(ctypes.c_void_p(256), 128, ctypes.c_void_p(256), 128,
+                                        None, 0, 4, 1000, 128, ctypes.c_void_p(256), None,
+                                        ctypes.c_void_p(256), None, None, 0, 0, None) \
+        == _lib.ERR_BAD_DTYPE  # fp32 operands
+    assert lib.areal_linear_logprob_scratch_bytes(1000, 151936) == 1000 * 75 * 2 * 16
 
 
 def test_minibatch_items_matches_reference_split():
