@@ -86,7 +86,7 @@ __device__ __forceinline__ void load_values(const uint4* q, int warp, int lane, 
                                             typename Traits<T>::Acc* f) {
   using A = typename Traits<T>::Acc;
   constexpr int E = Vec<T>::N;
-  if (nvec == kChunkBytes / 16) {  // full chunk: branch-free
+  if ((warp + 1) * (kWarpBytes / 16) <= nvec) {  // this warp's 2 KB all valid: branch-free
 #pragma unroll
     for (int j = 0; j < kVecPerThread; ++j) {
       A g[E];
@@ -507,10 +507,11 @@ __device__ __forceinline__ void row_ring_body(const PpoArgs& a) {
               if (vi < nvec) q[vi] = make_uint4(0, 0, 0, 0);
             }
           } else {
+            const bool wfull = (warp + 1) * (kWarpBytes / 16) <= nvec;  // this warp's 2 KB
 #pragma unroll
             for (int j = 0; j < kVecPerThread; ++j) {
               const int vi = vec_index(warp, lane, j);
-              if (nvec == kChunkBytes / 16 || vi < nvec) {
+              if (wfull || vi < nvec) {
                 A f[E];
                 Vec<T>::unpack(q[vi], f);
                 if constexpr (std::is_same<A, float>::value) {

@@ -211,7 +211,7 @@ __device__ __forceinline__ float fold_to_e(RowStat<float>& rs, uint32_t (&w)[16]
 template <typename T, bool ENT>
 __device__ __forceinline__ float chunk_to_e(RowStat<float>& rs, const uint4* q, uint32_t (&wv)[16],
                                             int warp, int lane, int nvec) {
-  if (nvec == kChunkBytes / 16) {
+  if ((warp + 1) * (kWarpBytes / 16) <= nvec) {  // this warp's region all valid
     lds_raw<true>(q, warp, lane, nvec, wv);
     return fold_to_e<T, ENT, true>(rs, wv, warp, lane, nvec);
   }
@@ -459,8 +459,8 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
       } else {
       Cursor c2 = cur;
       for (int c = 0; c < nchunks; ++c) {
-        const bool full = c < nfull;
-        const int nvec = (full ? kChunkBytes : last_bytes) / 16;
+        const int nvec = (c < nfull ? kChunkBytes : last_bytes) / 16;
+        const bool full = (warp + 1) * (kWarpBytes / 16) <= nvec;  // this warp's region
         uint32_t wv[16];
         if (c < ntm) {
           tmem_ld16(tmem_addr(tbase, warp, c), wv);
