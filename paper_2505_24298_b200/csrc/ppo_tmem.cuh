@@ -52,6 +52,15 @@ __device__ __forceinline__ float warp_max_redux(float v) {
 #endif
 constexpr bool kFixedShift = AREAL_K2_FIXED_SHIFT != 0;
 
+// Upper bound on the lookahead chunks folded during the per-row epilogue.  Fewer
+// lookahead chunks leave more ring slots to the producer during pass 2, so the read
+// stream keeps flowing while dlogits are written: 3 measured best at the power cap
+// (profiles/r01_k2_lookahead_sweep.txt: 6.27 vs 5.98 TB/s sustained at 5).
+#ifndef AREAL_K2_LA_CAP
+#define AREAL_K2_LA_CAP 3
+#endif
+constexpr int kLookaheadCap = AREAL_K2_LA_CAP;
+
 #ifndef AREAL_K2_PACKED_BF16_MUL
 #define AREAL_K2_PACKED_BF16_MUL 1
 #endif
@@ -238,7 +247,8 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
   const int nchunks = nfull + (last_bytes > 0 ? 1 : 0);
   const int ntm = min(nchunks, kTmemChunks);     // chunks parked in TMEM
   const int R = nchunks - ntm;                   // resident tail chunks
-  const int la_max = min(min((int)nslots - R, (int)nslots + kTmemChunks - nchunks), nchunks);
+  const int la_max = min(min(min((int)nslots - R, (int)nslots + kTmemChunks - nchunks), nchunks),
+                         kLookaheadCap);
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
