@@ -61,13 +61,6 @@ constexpr bool kFixedShift = AREAL_K2_FIXED_SHIFT != 0;
 #endif
 constexpr int kLookaheadCap = AREAL_K2_LA_CAP;
 
-// Park the next row's lookahead chunks in TMEM during this row's pass 2 (right after
-// the warp has read the TMEM region they go to) rather than at the next row's start.
-#ifndef AREAL_K2_PARK_IN_PASS2
-#define AREAL_K2_PARK_IN_PASS2 0
-#endif
-constexpr bool kParkInPass2 = AREAL_K2_PARK_IN_PASS2 != 0;
-
 #ifndef AREAL_K2_PACKED_BF16_MUL
 #define AREAL_K2_PACKED_BF16_MUL 1
 #endif
@@ -370,11 +363,8 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
       const int par = it & 1;
       float* cw = &tail->cw[par][0][0];  // [chunk][warp]
       // ---- park the lookahead chunks (their e is in the ring slots) in TMEM
-      // (kParkInPass2: already done during the previous row's pass 2)
       Cursor cc = cur;
-      if (kParkInPass2) {
-        for (int c = 0; c < la; ++c) cc.next(nslots);
-      } else for (int c = 0; c < la; ++c) {
+      for (int c = 0; c < la; ++c) {
         const int nvec = (c < nfull ? kChunkBytes : last_bytes) / 16;
         uint32_t wv[16];
         lds_raw(reinterpret_cast<const uint4*>(ring + (size_t)cc.slot * kChunkBytes), warp, lane,
@@ -433,20 +423,6 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
 
       mbar_wait(&tail->bcbar[par], (it >> 1) & 1);
       const RingBcast b = tail->bc[par];
-      // park lookahead chunk c of the next row (its e sits in ring position after + c)
-      // into TMEM chunk c, whose region this warp has already read in pass 2; frees the
-      // ring slot a row earlier than parking at the next row's start would
-      Cursor pk = after;
-      auto park_next = [&](int c) {
-        const int nvec = (c < nfull ? kChunkBytes : last_bytes) / 16;
-        uint32_t wv[16];
-        lds_raw(reinterpret_cast<const uint4*>(ring + (size_t)pk.slot * kChunkBytes), warp, lane,
-                nvec, wv);
-        tmem_st16(tmem_addr(tbase, warp, c), wv);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[pk.slot]);
-        pk.next(nslots);
-      };
       const float g = (float)b.gc;
       const float lse_s = (float)b.lse;
       const T dtok = from_bits<T>(b.dtok);
@@ -490,8 +466,6 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
           }
           cs.next(nslots);
         }
-        if (kParkInPass2)
-          for (int c = 0; c < la_next; ++c) park_next(c);
       } else {
       Cursor c2 = cur;
       for (int c = 0; c < nchunks; ++c) {
@@ -544,7 +518,6 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
           for (int j = 0; j < kVecPerThread; ++j)
             if (vec_index(warp, lane, j) < nvec) scale_store(j);
         }
-        if (kParkInPass2 && c < la_next) park_next(c);  // la_next <= ntm
         c2.next(nslots);
       }
       }  // fast path
