@@ -35,8 +35,8 @@ constexpr int BM = 128;            // tokens per tile (TMEM lanes)
 constexpr int BN = 256;            // vocab columns per MMA / accumulator
 constexpr int BK = 64;             // k-slab: 64 x 2 B = one 128-byte swizzle row
 constexpr int UMMA_K = 16;         // K per tcgen05.mma for 16-bit inputs
-constexpr int NT = 8;              // N-tiles per unit
-constexpr int VB = NT * BN;        // vocab block per unit
+constexpr int kMaxNT = 8;          // N-tiles per unit (runtime a.nt in {4, 8}; vocab block = nt * BN)
+constexpr int kMinNT = 4;          // sizes the partials scratch
 constexpr int A_BYTES = BM * BK * 2;
 constexpr int EPI_SPLIT = 2;       // epilogue warps per TMEM lane quarter (column halves)
 constexpr int EPI_THREADS = 128 * EPI_SPLIT;
@@ -52,6 +52,7 @@ struct Args {
   int64_t n_rows, vocab;
   int32_t dim, n_mt, n_vb, n_units;
   int32_t group;  // vocab blocks interleaved per token tile (L2 working-set shaping)
+  int32_t nt, vb;  // N-tiles per unit, vocab block = nt * BN columns
   uint32_t idesc;
 };
 
@@ -128,7 +129,7 @@ __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.
 // Unit u -> (token tile, vocab block).  `group` consecutive units share a token tile
 // and take `group` different vocab blocks, so the ~74 units in flight touch
 // 74/group H tiles and `group` W blocks: the L2 working set is
-// (74/group)*TM*d*2 + group*VB*d*2 bytes instead of 74*TM*d*2 (which exceeds L2
+// (74/group)*TM*d*2 + group*vb*d*2 bytes instead of 74*TM*d*2 (which exceeds L2
 // at d = 3584).  Units whose block lies past the vocab are empty.
 struct UnitXY { int mt, vb; };
 __device__ __forceinline__ UnitXY unit_xy(const Args& a, int u) {
@@ -241,8 +242,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         const UnitXY xy = unit_xy(a, u);
         const int mt = xy.mt, vb = xy.vb;
         const int32_t arow = mt * G::TM + (int32_t)rank * BM;
-        for (int n = 0; n < NT; ++n) {
-          const int64_t n0 = (int64_t)vb * VB + (int64_t)n * BN;
+        for (int n = 0; n < a.nt; ++n) {
+          const int64_t n0 = (int64_t)vb * a.vb + (int64_t)n * BN;
           if (n0 >= a.vocab) break;
           const int32_t brow = (int32_t)n0 + (int32_t)rank * G::B_ROWS;
           for (int ks = 0; ks < ksteps; ++ks) {
@@ -270,8 +271,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       uint32_t acc = 0, acc_phase = 0;
       for (int u = unit0; u < a.n_units; u += nunit_step) {
         const int vb = unit_xy(a, u).vb;
-        for (int n = 0; n < NT; ++n) {
-          const int64_t n0 = (int64_t)vb * VB + (int64_t)n * BN;
+        for (int n = 0; n < a.nt; ++n) {
+          const int64_t n0 = (int64_t)vb * a.vb + (int64_t)n * BN;
           if (n0 >= a.vocab) break;
           if constexpr (CG == 2) mbar_wait_cluster(&tempty[acc], acc_phase ^ 1u);
           else mbar_wait(&tempty[acc], acc_phase ^ 1u);
@@ -319,7 +320,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint32_t acc = 0, acc_phase = 0, bpar = 0;
     constexpr float L2E = 1.4426950408889634f;
     // iteration order of (unit, N-tile) pairs, identical to the producer / MMA loops
-    auto tile_n0 = [&](int u, int n) -> int64_t { return (int64_t)unit_xy(a, u).vb * VB + (int64_t)n * BN; };
+    auto tile_n0 = [&](int u, int n) -> int64_t { return (int64_t)unit_xy(a, u).vb * a.vb + (int64_t)n * BN; };
     auto load_bias = [&](int64_t n0) -> float2 {
       float2 b2 = make_float2(0.f, 0.f);
       if (a.bias != nullptr && n0 >= 0) {
@@ -343,12 +344,12 @@ __global__ void __launch_bounds__(THREADS, 1)
         tok = a.tokens[idx];
       }
       float m = -INFINITY, s = 0.f, sx = 0.f, xa = 0.f;
-      for (int n = 0; n < NT; ++n) {
+      for (int n = 0; n < a.nt; ++n) {
         const int64_t n0 = tile_n0(u, n);
         if (n0 >= a.vocab) break;
         // prefetch the biases of the next (unit, N-tile) in iteration order
         int64_t nn0 = -1;
-        if (n + 1 < NT && tile_n0(u, n + 1) < a.vocab) nn0 = tile_n0(u, n + 1);
+        if (n + 1 < a.nt && tile_n0(u, n + 1) < a.vocab) nn0 = tile_n0(u, n + 1);
         else if (u + nunit_step < a.n_units) nn0 = tile_n0(u + nunit_step, 0);
         const float2 bnext = load_bias(nn0);
         const float* bs = sbias[bpar];
@@ -445,7 +446,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 }
 
 // One warp per row: merge the row's block partials in block order.
-__global__ void linear_lp_merge_kernel(const float4* partials, int n_vb, int64_t n_rows, int64_t vocab,
+__global__ void linear_lp_merge_kernel(const float4* partials, int n_vb, int vblock, int64_t n_rows,
+                                       int64_t vocab,
                                        const int64_t* tokens, const int32_t* row_index, double* lp,
                                        double* ent) {
   const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -465,7 +467,7 @@ __global__ void linear_lp_merge_kernel(const float4* partials, int n_vb, int64_t
     const double lse = (double)w.m + log((double)w.s);
     double xa = nan("");
     if (tok >= 0 && tok < vocab)  // the partial of the (block, column slice) holding the token
-      xa = (double)partials[(row * n_vb + tok / VB) * EPI_SPLIT + (int)((tok % BN) / (BN / EPI_SPLIT))].w;
+      xa = (double)partials[(row * n_vb + tok / vblock) * EPI_SPLIT + (int)((tok % BN) / (BN / EPI_SPLIT))].w;
     lp[idx] = xa - lse;
     if (ent) ent[idx] = lse - (double)w.sx / (double)w.s;
   }
@@ -505,7 +507,8 @@ static bool make_map(CUtensorMap* map, const void* base, CUtensorMapDataType dt,
 using namespace areal;
 
 extern "C" size_t areal_linear_logprob_scratch_bytes(int64_t n_rows, int64_t vocab) {
-  const int64_t n_vb = (vocab + k7::VB - 1) / k7::VB;
+  const int64_t vbmin = (int64_t)k7::kMinNT * k7::BN;  // smallest vocab block -> most partials
+  const int64_t n_vb = (vocab + vbmin - 1) / vbmin;
   return (size_t)(n_rows > 0 ? n_rows : 0) * (size_t)n_vb * k7::EPI_SPLIT * sizeof(float4);
 }
 
@@ -525,7 +528,7 @@ extern "C" int areal_linear_logprob_fwd(const void* hidden, int64_t ld_hidden, c
       reinterpret_cast<uintptr_t>(hidden) % 16 || reinterpret_cast<uintptr_t>(weight) % 16 ||
       (bias && reinterpret_cast<uintptr_t>(bias) % 16))
     return AREAL_ERR_MISALIGNED;
-  if (n_rows > ((int64_t)1 << 31) - BM || vocab > ((int64_t)1 << 31) - VB) return AREAL_ERR_BAD_SHAPE;
+  if (n_rows > ((int64_t)1 << 31) - BM || vocab > ((int64_t)1 << 31) - kMaxNT * BN) return AREAL_ERR_BAD_SHAPE;
   if (!scratch || scratch_bytes < areal_linear_logprob_scratch_bytes(n_rows, vocab)) return AREAL_ERR_WORKSPACE;
   const CUtensorMapDataType dt = dtype == AREAL_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   CUtensorMap tmA, tmB;
@@ -537,7 +540,6 @@ extern "C" int areal_linear_logprob_fwd(const void* hidden, int64_t ld_hidden, c
   a.n_rows = n_rows;
   a.vocab = vocab;
   a.dim = (int32_t)dim;
-  a.n_vb = (int32_t)((vocab + VB - 1) / VB);
   // kind::f16 instruction descriptor: D fp32, A/B bf16 (1) or fp16 (0), both K-major,
   // N >> 3 at bit 17, M >> 4 at bit 24 (cute::UMMA::InstrDescriptor)
   const uint32_t ab = dtype == AREAL_BF16 ? 1u : 0u;
@@ -550,17 +552,25 @@ extern "C" int areal_linear_logprob_fwd(const void* hidden, int64_t ld_hidden, c
   const int tm = BM * cg;
   a.n_mt = (int32_t)((n_rows + tm - 1) / tm);
   {
-    // group: minimise the L2 working set of the units in flight (see unit_xy)
+    // group: minimise the L2 working set of the units in flight, (in_flight / group)
+    // H tiles + group W blocks of nt * 256 columns (see unit_xy).  nt = 8 N-tiles per
+    // unit; 4 (smaller W blocks, AREAL_K7_NT=4) measured no faster at d = 1536 / 3584
+    // (profiles/r01_k7_nt_group_sweep.txt)
     const double in_flight = cg == 2 ? sms / 2 : sms;
-    int best = 1;
+    int best_g = 1, best_nt = kMaxNT;
     double best_bytes = 1e300;
-    for (int gsz = 1; gsz <= 8; gsz *= 2) {
-      const double bytes = (in_flight / gsz) * tm * (double)dim * 2 + gsz * (double)VB * dim * 2;
-      if (bytes < best_bytes) best = gsz, best_bytes = bytes;
+    for (int gsz = 1; gsz <= 16; gsz *= 2) {
+      const double bytes = (in_flight / gsz) * tm * (double)dim * 2 + gsz * (double)best_nt * BN * dim * 2;
+      if (bytes < best_bytes - 1.0) best_g = gsz, best_bytes = bytes;
     }
+    const char* env_nt = getenv("AREAL_K7_NT");
+    if (env_nt && (atoi(env_nt) == 4 || atoi(env_nt) == 8)) best_nt = atoi(env_nt);
     const char* env = getenv("AREAL_K7_GROUP");
-    if (env && atoi(env) >= 1) best = atoi(env);
-    a.group = std::min(best, (int)a.n_vb);
+    if (env && atoi(env) >= 1) best_g = atoi(env);
+    a.nt = best_nt;
+    a.vb = best_nt * BN;
+    a.n_vb = (int32_t)((vocab + a.vb - 1) / a.vb);
+    a.group = std::min(best_g, (int)a.n_vb);
   }
   a.n_units = a.n_mt * ((a.n_vb + a.group - 1) / a.group) * a.group;
   a.idesc = (1u << 4) | (ab << 7) | (ab << 10) | ((uint32_t)(BN >> 3) << 17) |
@@ -594,7 +604,7 @@ extern "C" int areal_linear_logprob_fwd(const void* hidden, int64_t ld_hidden, c
   AREAL_CUDA_CHECK_LAUNCH();
   const int64_t threads = n_rows * 32;
   linear_lp_merge_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, stream>>>(
-      a.partials, a.n_vb, n_rows, vocab, tokens, row_index, lp_out, entropy_out);
+      a.partials, a.n_vb, a.vb, n_rows, vocab, tokens, row_index, lp_out, entropy_out);
   AREAL_CUDA_CHECK_LAUNCH();
   return AREAL_OK;
 }

@@ -72,7 +72,7 @@ def test_library_validates_without_gpu():
                                         None, 0, 4, 1000, 128, ctypes.c_void_p(256), None,
                                         ctypes.c_void_p(256), None, None, 0, 0, None) \
         == _lib.ERR_BAD_DTYPE  # fp32 operands
-    assert lib.areal_linear_logprob_scratch_bytes(1000, 151936) == 1000 * 75 * 2 * 16
+    assert lib.areal_linear_logprob_scratch_bytes(1000, 151936) == 1000 * 149 * 2 * 16
 
 
 def test_minibatch_items_matches_reference_split():
