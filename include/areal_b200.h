@@ -192,7 +192,8 @@ int areal_fill_gather(const int64_t* traj_bounds, const int32_t* packed_traj,
  * row_index[r] (NULL = r): lp_out[idx] = x[tok] - logsumexp(x), entropy_out (may be
  * NULL) = -sum p log p, x = hidden[r] . weight^T + bias accumulated in fp32 on the
  * tensor cores.  The [n_rows, vocab] logits never reach HBM.  scratch (device) holds
- * per-(row, 2048-column block) partials: areal_linear_logprob_scratch_bytes().
+ * per-(row, vocab block, column half) partials: areal_linear_logprob_scratch_bytes()
+ * (sized for the smallest vocab block, 1024 columns; 32 B per row per block).
  * cta_group: 1 = one CTA per 128-token tile (tcgen05 .cta_group::1, M=128),
  * 2 = a CTA pair per 256-token tile (.cta_group::2, M=256, each CTA loads half of the
  * W tile), 0 = choose (2 when n_rows > 128). */
