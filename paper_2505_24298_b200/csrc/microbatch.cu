@@ -36,12 +36,12 @@ struct PlanArgs {
 };
 
 // warp-cooperative exclusive scan of src[0..n) into dst[0..n], dst[n] = total
-template <typename V>
-__device__ void warp_exclusive_scan(const V* src, V* dst, int n, int lane) {
+template <typename S, typename V>
+__device__ void warp_exclusive_scan(const S* src, V* dst, int n, int lane) {
   V carry = 0;
   for (int base = 0; base < n; base += 32) {
     const int i = base + lane;
-    V v = (i < n) ? src[i] : V(0);
+    V v = (i < n) ? (V)src[i] : V(0);
     V x = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -54,19 +54,31 @@ __device__ void warp_exclusive_scan(const V* src, V* dst, int n, int lane) {
   if (lane == 0) dst[n] = carry;
 }
 
+// Region A of the plan kernel's shared memory: the sort keys, later the group prefix
+// sums (int64 token starts + int32 item starts), 16-byte aligned.
+__host__ __device__ inline size_t plan_region_a(int n, int npow2) {
+  const size_t keys = (size_t)npow2 * 8, sums = (size_t)(n + 1) * 12;
+  return ((keys > sums ? keys : sums) + 15) & ~(size_t)15;
+}
+
 __global__ void __launch_bounds__(kPlanThreads) plan_kernel(PlanArgs a, int npow2) {
   extern __shared__ __align__(16) unsigned char sm[];
   const int m = blockIdx.x;
   const int off = a.mb_offsets[m];
   const int n = a.mb_offsets[m + 1] - off;
-  uint64_t* keys = reinterpret_cast<uint64_t*>(sm);             // [npow2]
-  int64_t* tot = reinterpret_cast<int64_t*>(keys + npow2);      // [n + 1] group token totals -> starts
-  int64_t* gstart = tot + (n + 1);                              // [n + 1]
-  int32_t* cnt = reinterpret_cast<int32_t*>(gstart + (n + 1));  // [n + 1] group member counts
-  int32_t* gis = cnt + (n + 1);                                 // [n + 1] group item starts
-  int32_t* gof = gis + (n + 1);                                 // [n] group of item
-  int32_t* slt = gof + n;                                       // [n] slot of item
-  int64_t* ofs = reinterpret_cast<int64_t*>(slt + n);         // [n] token offset in group (4n+2 int32s above: 8B aligned)
+  // shared memory (plan_smem): region A holds the sort keys until placement is done,
+  // then the group prefix sums; totals / counts / in-group offsets are 32-bit (each
+  // <= capacity < 2^31); an item's group and slot go straight to the global outputs.
+  // 196 KB at the 8,192-item maximum.
+  const size_t region_a = plan_region_a(n, npow2);
+  uint64_t* keys = reinterpret_cast<uint64_t*>(sm);                   // [npow2]      (region A)
+  int64_t* gstart = reinterpret_cast<int64_t*>(sm);                   // [n + 1]      (region A, later)
+  int32_t* gis = reinterpret_cast<int32_t*>(gstart + (n + 1));        // [n + 1]      (region A, later)
+  int32_t* tot = reinterpret_cast<int32_t*>(sm + region_a);           // [n + 1] group token totals
+  int32_t* cnt = tot + (n + 1);                                       // [n + 1] group member counts
+  int32_t* ofs = cnt + (n + 1);                                       // [n] token offset in group
+  int32_t* gof = a.group_of + off;                                    // [n] (global output)
+  int32_t* slt = a.slot_of + off;                                     // [n] (global output)
   __shared__ int s_bad_idx, s_bad_code, s_G;
   const int tid = threadIdx.x, lane = tid & 31;
   if (tid == 0) {
@@ -140,7 +152,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(PlanArgs a, int npow
       uint32_t best = 0xffffffffu;
       if (G >= kmin) {
         for (int g = lane; g < G; g += 32) {
-          if (tot[g] + s <= C) {
+          if ((int64_t)tot[g] + s <= C) {
             const uint32_t kk = ((uint32_t)cnt[g] << 13) | (uint32_t)g;
             best = kk < best ? kk : best;
           }
@@ -159,7 +171,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(PlanArgs a, int npow
         gof[item] = g;
         slt[item] = cnt[g];
         ofs[item] = tot[g];
-        tot[g] += s;
+        tot[g] += (int32_t)s;
         cnt[g] += 1;
       }
       if (best == 0xffffffffu) ++G;
@@ -170,8 +182,9 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(PlanArgs a, int npow
   __syncthreads();
   const int G = s_G;
   // ---- offsets: token starts and item starts of each group
-  if (tid < 32) warp_exclusive_scan<int64_t>(tot, gstart, G, lane);
-  else if (tid < 64) warp_exclusive_scan<int32_t>(cnt, gis, G, lane);
+  // region A is free now (keys dead after placement); scans of the group totals / counts
+  if (tid < 32) warp_exclusive_scan<int32_t, int64_t>(tot, gstart, G, lane);
+  else if (tid < 64) warp_exclusive_scan<int32_t, int32_t>(cnt, gis, G, lane);
   __syncthreads();
   const int64_t t0 = a.mb_token_start[m];
   const int base = off + m;  // this minibatch's slice of group_cu / group_seq_cu
@@ -181,8 +194,6 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(PlanArgs a, int npow
   }
   for (int i = tid; i < n; i += blockDim.x) {
     const int g = gof[i];
-    a.group_of[off + i] = g;
-    a.slot_of[off + i] = slt[i];
     const int pos = off + gis[g] + slt[i];
     a.packed_traj[pos] = a.item_traj[off + i];
     a.seq_cu[pos] = t0 + gstart[g] + ofs[i];
@@ -215,8 +226,7 @@ __global__ void fill_gather_kernel(const int64_t* bounds, const int32_t* packed_
 }
 
 static size_t plan_smem(int n, int npow2) {
-  return (size_t)npow2 * 8 + 2 * (size_t)(n + 1) * 8 + 2 * (size_t)(n + 1) * 4 + 2 * (size_t)n * 4 +
-         (size_t)n * 8 + 64;
+  return plan_region_a(n, npow2) + 2 * (size_t)(n + 1) * 4 + (size_t)n * 4 + 64;
 }
 
 }  // namespace areal

@@ -484,3 +484,26 @@ def test_ppo_prox_from_lp(dt, V, algo):
     assert ok, err
     s = st.cpu().numpy()
     assert abs(s[3] - s[1]) <= 1e-9 * max(1.0, s[1])  # every valid ratio is exactly 1
+
+
+def test_allocator_max_items_and_limits():
+    """The largest minibatch the allocator takes (AREAL_MAX_ITEMS_PER_MINIBATCH = 8192
+    sequences) is bit-exact vs the oracle (Alg. 1, trainer.py:235-270); one more is
+    rejected on the host; heavy ties and k_min > n behave like the reference."""
+    from paper_2505_24298_b200 import _lib
+    rng = np.random.default_rng(99)
+    n = _lib.MAX_ITEMS_PER_MINIBATCH
+    lengths = rng.integers(1, 200, size=n)
+    lengths[::7] = 50  # many ties: stable order by index (trainer.py:253)
+    plan, _ = _plan_one(lengths, 4096, 16)
+    ref = O.allocate_microbatches([int(x) for x in lengths], 4096, 16)
+    gid = plan.group_of.cpu().numpy()
+    slot = plan.slot_of.cpu().numpy()
+    got = [[] for _ in range(int(plan.n_groups[0]))]
+    for i in np.argsort(slot, kind="stable"):
+        got[gid[i]].append(int(i))
+    assert [list(g) for g in ref] == got
+    with pytest.raises(ValueError):
+        _plan_one(np.ones(n + 1, dtype=np.int64), 4096, 1)
+    plan, _ = _plan_one([2, 2, 2], 10, 8)  # k_min > n: every item its own group
+    assert int(plan.n_groups[0]) == 3
