@@ -507,3 +507,19 @@ def test_allocator_max_items_and_limits():
         _plan_one(np.ones(n + 1, dtype=np.int64), 4096, 1)
     plan, _ = _plan_one([2, 2, 2], 10, 8)  # k_min > n: every item its own group
     assert int(plan.n_groups[0]) == 3
+
+
+@pytest.mark.parametrize("dt,V", [("bf16", 262144), ("f32", 151936), ("bf16", 229376),
+                                  ("f16", 200003)])
+def test_large_vocab_paths(dt, V):
+    """Rows beyond the TMEM kernel's 14 x 32 KB (bf16 V > 229,376; fp32 V > 114,688)
+    fall back to the cluster-split ring; both sides of the boundary and an odd V
+    match the float64 oracle (K1 and K2)."""
+    T = 12
+    logits, x64, tokens, behav, prox, adv = make_case(T, V, dt, seed=V % 97)
+    lp, ent = K.logprob_fwd(logits.cuda(), cuda(tokens))
+    ok, err = rel_close(lp.cpu().numpy(), O.token_logprobs(x64, tokens), TOL[dt])
+    assert ok, err
+    dl, st = K.ppo_fwd_bwd(logits.cuda(), cuda(tokens), cuda(behav), cuda(prox), cuda(adv))
+    ref = O.surrogate_terms(x64, tokens, behav, prox, adv)
+    check_k2(dt, dl.double().cpu().numpy(), st.cpu().numpy(), ref, T)
