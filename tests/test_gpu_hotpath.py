@@ -193,3 +193,24 @@ def test_fused_first_prox_matches_unfused():
     assert np.array_equal(s0[:, counts], s1[:, counts])
     np.testing.assert_allclose(s1, s0, rtol=2e-2, atol=1e-6)
     np.testing.assert_allclose(p1, p0, rtol=0, atol=2e-5)
+
+
+def test_run_degenerate_batches():
+    """Empty trajectories only, fewer trajectories than minibatches, a single token:
+    the step completes with the reference's counts (trainer.py:300-315: empty chunks
+    and zero-length trajectories are dropped)."""
+    V = 512
+    table = torch.randn(4, V, device="cuda").to(torch.bfloat16)
+    lf = lambda ph, m, g, rows: table.index_select(0, rows.long())
+    # all trajectories empty
+    ro = PackedRollouts.from_host(np.array([0, 0, 0], dtype=np.int64), np.zeros(0, np.int64),
+                                  np.zeros(0), np.array([1.0, -1.0]))
+    res = DecoupledPPOStep(HotPathConfig(minibatches=4)).run(ro, lf)
+    assert res.minibatch_updates == 0 and res.tokens == 0
+    # 3 trajectories, 4 minibatches (array_split leaves one chunk empty), 4 tokens total
+    bounds = np.array([0, 1, 3, 4], dtype=np.int64)
+    ro = PackedRollouts.from_host(bounds, np.array([1, 2, 3, 4]), np.full(4, -6.0),
+                                  np.array([5.0, -5.0, 5.0]))
+    res = DecoupledPPOStep(HotPathConfig(minibatches=4)).run(ro, lf)
+    assert res.minibatch_updates == 3 and res.tokens == 4
+    assert res.minibatch_stats[:, 7].sum() == 4
