@@ -274,6 +274,35 @@ class LossResult:
     excluded: int
 
 
+def _surrogate_terms(batch: TrainBatch, idx, params, clip_eps: float, decoupled: bool):
+    """trainer.py:150-195: objective and gradient sums over one token subset (K2 + the
+    linear policy's GEMMs), as raw sums so micro-batch accumulation stays exact."""
+    if batch.prox_logprobs is None or batch.advantages is None:
+        raise BatchError("populate prox_logprobs and advantages before the loss")
+    dev = _device()
+    idx = np.asarray(idx, dtype=np.int64)
+    X = _d(batch.features[idx], torch.float64, dev)
+    W = _d(params.weights, torch.float64, dev)
+    b = _d(params.bias, torch.float64, dev)
+    stats = torch.zeros(8, dtype=torch.float64, device=dev)
+    if len(idx):
+        logits = _linear_logits(X, W, b)
+        dl, stats = K.ppo_fwd_bwd(logits, _d(batch.tokens[idx], torch.int64, dev),
+                                  _d(batch.behavior_logprobs[idx], torch.float64, dev),
+                                  _d(batch.prox_logprobs[idx], torch.float64, dev),
+                                  _d(batch.advantages[idx], torch.float64, dev),
+                                  clip_eps=clip_eps, decoupled=decoupled, stats=stats,
+                                  dlogits=logits)
+        # dl = coef (softmax - onehot) = -resid, so resid^T feats = -(dl^T X) (exact negation)
+        gw, gb = -(dl.t() @ X), -dl.sum(dim=0)
+    else:
+        gw, gb = torch.zeros_like(W), torch.zeros_like(b)
+    s = stats.cpu().numpy()
+    return {"objective_sum": float(s[0]), "grad_w_sum": gw.cpu().numpy(),
+            "grad_b_sum": gb.cpu().numpy(), "n_valid": int(s[1]), "n_clipped": int(s[2]),
+            "ratio_sum": float(s[3]), "n_excluded": int(s[4])}
+
+
 def _ppo_loss(batch: TrainBatch, params, clip_eps: float, decoupled: bool) -> LossResult:
     """trainer.py:198-213: whole-batch loss via one K2 launch."""
     if batch.prox_logprobs is None or batch.advantages is None:

@@ -124,3 +124,21 @@ def test_train_step_deterministic():
         outs.append(newp)
     assert np.array_equal(outs[0].weights, outs[1].weights)
     assert np.array_equal(outs[0].bias, outs[1].bias)
+
+
+def test_surrogate_terms_mirror_matches_loss():
+    # _surrogate_terms (trainer.py:150-195) over all tokens == _ppo_loss's raw sums
+    c = load_cases("trainstep.npz")[0]
+    batch = _batch(c)
+    batch.prox_logprobs = c["dec_prox"]
+    T.compute_advantages(batch)
+    params = T.VersionedParams(1, c["W"], c["b"])
+    t = T._surrogate_terms(batch, np.arange(batch.n_tokens), params, float(c["clip_eps"]), True)
+    r = T.decoupled_ppo_loss(batch, params, clip_eps=float(c["clip_eps"]))
+    n = max(t["n_valid"], 1)
+    assert t["n_valid"] == r.n_tokens and t["n_excluded"] == r.excluded
+    assert -t["objective_sum"] / n == pytest.approx(r.loss, rel=1e-12, abs=1e-14)
+    assert np.allclose(-t["grad_w_sum"] / n, r.grad.weights, rtol=1e-12, atol=1e-15)
+    assert np.allclose(c["dec_gw"], r.grad.weights, rtol=1e-10, atol=1e-13)
+    empty = T._surrogate_terms(batch, np.zeros(0, dtype=np.int64), params, 0.2, True)
+    assert empty["n_valid"] == 0 and empty["objective_sum"] == 0.0
