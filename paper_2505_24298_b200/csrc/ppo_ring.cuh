@@ -120,6 +120,13 @@ __device__ __forceinline__ void load_values(const uint4* q, int warp, int lane, 
 #endif
 constexpr bool kK1ArriveAllLanes = AREAL_K1_ARRIVE_ALL_LANES != 0;
 
+// Math warps fold their 32 lanes' row statistics with one max, one rescale exp per
+// lane and sum butterflies (warp_merge) instead of five pairwise merge rounds.
+#ifndef AREAL_MATH_WARP_MERGE
+#define AREAL_MATH_WARP_MERGE 1
+#endif
+constexpr bool kMathWarpMerge = AREAL_MATH_WARP_MERGE != 0;
+
 #ifndef AREAL_POLY_EVERY
 #define AREAL_POLY_EVERY 8
 #endif
@@ -234,22 +241,27 @@ __device__ __forceinline__ void fold_values(RowStat<typename Traits<T>::Acc>& rs
 // Merge the warp's per-lane partials into one (max, sum, sum*x), identical on every
 // lane: max-reduce, one rescale exp per lane, then two sum-reduces (XOR
 // butterflies, fixed order => deterministic and bitwise equal across lanes).
-template <typename A>
-__device__ __forceinline__ RowStat<A> warp_merge(const RowStat<A>& w) {
+template <typename A, bool ENT>
+__device__ __forceinline__ RowStat<A> warp_merge_ent(const RowStat<A>& w) {
   const A M = warp_max(w.m);
   const A muse = (M == Lim<A>::ninf()) ? A(0) : M;
   const A f = (w.m == Lim<A>::ninf()) ? A(0) : Ex<A>::e(w.m, Ex<A>::shift(muse));
-  A s = w.s * f, sx = w.sx * f;
+  A s = w.s * f, sx = ENT ? w.sx * f : A(0);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     s += __shfl_xor_sync(0xffffffffu, s, o);
-    sx += __shfl_xor_sync(0xffffffffu, sx, o);
+    if (ENT) sx += __shfl_xor_sync(0xffffffffu, sx, o);
   }
   RowStat<A> r;
   r.m = M;
   r.s = s;
   r.sx = sx;
   return r;
+}
+
+template <typename A>
+__device__ __forceinline__ RowStat<A> warp_merge(const RowStat<A>& w) {
+  return warp_merge_ent<A, true>(w);
 }
 
 template <typename T> __device__ __forceinline__ unsigned long long to_bits(T v) {
@@ -454,7 +466,7 @@ __device__ __forceinline__ void row_ring_body(const PpoArgs& a) {
         cc.next(nslots);
       }
       const Cursor after = cc;  // ring position of the next row's chunk 0
-      rs.warp_reduce();
+      rs = kMathWarpMerge ? warp_merge_ent<A, ENT>(rs) : (rs.warp_reduce(), rs);
       // K1 flow control: never hand off row i+1 before the epilogue warp took row i
       // (K2 already waited for row i's coefficient before its pass 2)
       if (!BWD && it > 0) mbar_wait(&tail->bcbar[par ^ 1], ((it - 1) >> 1) & 1);

@@ -394,7 +394,7 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
       }
       const Cursor after = cc;
       tmem_wait_st();  // this row's parked chunks are in TMEM before pass 2 reads them
-      rs.warp_reduce();
+      rs = kMathWarpMerge ? warp_merge_ent<A, ENT>(rs) : (rs.warp_reduce(), rs);
       if (lane == 0) {
         tail->red[par][warp][0] = rs.m;
         tail->red[par][warp][1] = rs.s;
