@@ -5,17 +5,20 @@
 // (_surrogate_terms) and policy.py:145-163 (log_softmax, batch_token_log_probs),
 // restated on given logits; see DESIGN.md §3 for the data layout and rooflines.
 //
-// Two kernels per op:
+// Kernels (AREAL_ALGO_AUTO picks per shape):
 //   row_warp : one warp per row, any vocab / alignment; both passes read global
-//              memory (the second pass hits L1/L2).  Small-vocab and fallback path.
-//   row_ring : persistent, warp-specialised.  A producer thread streams the row
-//              through a ring of 16 KB shared-memory chunks with 1-D TMA bulk
-//              copies (cp.async.bulk + mbarrier complete_tx).  K2 keeps the whole
-//              row slice resident: pass 1 reduces (max, sum e^x, sum e^x*x) as
-//              chunks land, the CTAs of a thread-block cluster (which split the
-//              vocab) exchange their partials through DSMEM, pass 2 rewrites each
-//              chunk in place as dlogits and streams it out with a bulk store.
-//              HBM traffic = one logits read + one dlogits write per element.
+//              memory (the second pass hits L1/L2).  Small-vocab, unaligned and fp64.
+//   row_ring : persistent, warp-specialised (ppo_ring.cuh).  A producer thread
+//              streams each row through a ring of 32 KB shared-memory chunks with
+//              1-D TMA bulk copies (cp.async.bulk + mbarrier complete_tx).  K1 frees
+//              a chunk as soon as it is in registers; K2 keeps the row resident, and
+//              rows larger than the ring are split over a thread-block cluster whose
+//              CTAs exchange their partials through DSMEM; pass 2 rewrites each chunk
+//              in place as dlogits and bulk-stores it.
+//   tmem     : K2 for rows larger than one CTA's shared memory (ppo_tmem.cuh): the
+//              row's first 8 chunks are parked in Tensor Memory as e = 2^(x - c),
+//              the tail stays in the ring, one CTA per row (the bf16 V ~ 152K default).
+// HBM traffic = one logits read (+ one dlogits write for K2) per element.
 #include <cstdlib>
 #include <type_traits>
 
