@@ -62,8 +62,8 @@ typedef enum { AREAL_F32 = 0, AREAL_BF16 = 1, AREAL_F16 = 2, AREAL_F64 = 3 } are
 /* Kernel selection for K1/K2.  AUTO picks, for 16-byte-aligned rows: K2 on rows
  * larger than one CTA's shared memory -> the Tensor-Memory kernel (row parked in
  * TMEM, up to 14 x 32 KB), beyond that a thread-block-cluster split of ROW_RING;
- * smaller rows and all of K1 -> ROW_RING (TMA bulk ring); small or unaligned rows
- * and fp64 -> ROW_WARP (one warp per row). */
+ * smaller rows and all of K1 -> ROW_RING (TMA bulk ring); rows under 16 KB or
+ * unaligned -> ROW_WARP (one warp per row). */
 typedef enum { AREAL_ALGO_AUTO = 0, AREAL_ALGO_ROW_WARP = 1, AREAL_ALGO_ROW_RING = 2 } areal_algo_t;
 
 /* Order of the float64 statistics vector (accumulated with +=). */

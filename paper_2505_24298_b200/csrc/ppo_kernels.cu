@@ -7,7 +7,7 @@
 //
 // Kernels (AREAL_ALGO_AUTO picks per shape):
 //   row_warp : one warp per row, any vocab / alignment; both passes read global
-//              memory (the second pass hits L1/L2).  Small-vocab, unaligned and fp64.
+//              memory (the second pass hits L1/L2).  Rows under 16 KB or unaligned.
 //   row_ring : persistent, warp-specialised (ppo_ring.cuh).  A producer thread
 //              streams each row through a ring of 32 KB shared-memory chunks with
 //              1-D TMA bulk copies (cp.async.bulk + mbarrier complete_tx).  K1 frees
