@@ -35,6 +35,12 @@ constexpr int BM = 128;            // tokens per tile (TMEM lanes)
 constexpr int BN = 256;            // vocab columns per MMA / accumulator
 constexpr int BK = 64;             // k-slab: 64 x 2 B = one 128-byte swizzle row
 constexpr int UMMA_K = 16;         // K per tcgen05.mma for 16-bit inputs
+#ifndef K7_STAGES2
+#define K7_STAGES2 6   // pipeline stages of the CTA-pair kernel (32 KB each)
+#endif
+#ifndef K7_ALIGN_SLACK
+#define K7_ALIGN_SLACK 1024  // run-time 1024-B alignment slack for the swizzled stages
+#endif
 constexpr int kMaxNT = 8;          // N-tiles per unit (runtime a.nt in {4, 8}; vocab block = nt * BN)
 constexpr int kMinNT = 4;          // sizes the partials scratch
 constexpr int A_BYTES = BM * BK * 2;
@@ -156,8 +162,8 @@ struct Pipe {
 template <int CG> struct Geo {
   static constexpr int B_ROWS = BN / CG;                     // B rows loaded per CTA
   static constexpr int STAGE = A_BYTES + B_ROWS * BK * 2;    // bytes per stage per CTA
-  static constexpr int NSTAGE = (CG == 1) ? 4 : 6;
-  static constexpr int SMEM = NSTAGE * STAGE + 1024;
+  static constexpr int NSTAGE = (CG == 1) ? 4 : K7_STAGES2;
+  static constexpr int SMEM = NSTAGE * STAGE + K7_ALIGN_SLACK;
   static constexpr int TM = BM * CG;                         // tokens per unit
 };
 
@@ -191,7 +197,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     linear_lp_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const Args a) {
   using G = Geo<CG>;
-  extern __shared__ unsigned char smem_raw[];
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t full[G::NSTAGE], empty[G::NSTAGE], tfull[2], tempty[2];
