@@ -336,7 +336,7 @@ __device__ __forceinline__ void row_warp_body(const PpoArgs& a) {
 namespace areal {
 
 template <typename T, bool ENT>
-__global__ void __launch_bounds__(kRingThreads, 1) ppo_tmem_kernel(PpoArgs a) {
+__global__ void __launch_bounds__(kTThreads, 1) ppo_tmem_kernel(PpoArgs a) {
   if constexpr (sizeof(T) == 2 || sizeof(T) == 4) tmem_k2_body<T, ENT>(a);
 }
 
@@ -405,7 +405,7 @@ static int launch_tmem(PpoArgs a, cudaStream_t stream, const DevInfo& d, int nsl
     attr_set[dev] = 1;
   }
   const int64_t grid = std::min<int64_t>(a.n_rows, (int64_t)d.sms);  // one CTA (all of TMEM) per SM
-  kern<<<(unsigned)grid, kRingThreads, smem, stream>>>(a);
+  kern<<<(unsigned)grid, kTThreads, smem, stream>>>(a);
   AREAL_CUDA_CHECK_LAUNCH();
   return AREAL_OK;
 }

@@ -28,6 +28,25 @@
 namespace areal {
 
 constexpr int kTmemChunks = 8;        // 8 x 32 KB = the whole 256 KB of TMEM
+
+// Math-warp geometry of this kernel (independent of the ring kernel's): kTW warps
+// each own kTWBytes of every 32 KB chunk, i.e. kTV 16-byte vectors (kTWords 32-bit
+// words) per thread per chunk; in TMEM each warp holds kTWords columns of its lane
+// quarter per parked chunk (64 columns per chunk either way).
+#ifndef AREAL_TMEM_WARPS
+#define AREAL_TMEM_WARPS 16
+#endif
+constexpr int kTW = AREAL_TMEM_WARPS;
+static_assert(kTW == 8 || kTW == 16, "TMEM K2: 8 or 16 math warps");
+constexpr int kTWBytes = kChunkBytes / kTW;
+constexpr int kTV = kTWBytes / 16 / 32;
+constexpr int kTWords = kTV * 4;
+constexpr int kTProducer = kTW, kTEpilogue = kTW + 1;
+constexpr int kTThreads = kTW * 32 + 64;
+constexpr int kTBarThreads = (kTW + 1) * 32;
+__device__ __forceinline__ int t_vec_index(int warp, int lane, int j) {
+  return warp * (kTWBytes / 16) + j * 32 + lane;
+}
 // Warp max of a float through one REDUX.MAX on an order-preserving integer image
 // (one instruction instead of a 5-step shuffle/max chain on the per-chunk critical path).
 #ifndef AREAL_K2_REDUX_MAX
@@ -81,10 +100,10 @@ constexpr int kTmemMaxChunks = 14;    // kTmemChunks + (nslots - 1) with 7 slots
 
 struct TmemTail {
   uint64_t bcbar[2];                          // epilogue -> math warps (row parity)
-  float red[2][kConsumerWarps][3];            // per-warp partials (row parity)
+  float red[2][kTW][3];            // per-warp partials (row parity)
   RingBcast bc[2];
   double st[AREAL_N_STATS];
-  float cw[2][kTmemMaxChunks][kConsumerWarps];  // shift c of the stored e (row parity)
+  float cw[2][kTmemMaxChunks][kTW];  // shift c of the stored e (row parity)
 };
 
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
@@ -116,19 +135,55 @@ __device__ __forceinline__ void tmem_fence_after() {
 }
 
 // TMEM address of math warp `warp`'s part of parked chunk t: lane quarter
-// (warp % 4) in bits 31:16, 16 columns per warp, 4 warps per quarter per chunk.
+// (warp % 4) in bits 31:16, kTWords columns per warp, kTW/4 warps per quarter per chunk.
 __device__ __forceinline__ uint32_t tmem_addr(uint32_t base, int warp, int t) {
-  return base + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(t * 64 + (warp >> 2) * 16);
+  return base + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(t * 64 + (warp >> 2) * kTWords);
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, "
+      "%29, %30, %31, %32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+      "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]),
+      "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]),
+      "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld32w(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, "
+      "%30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr)
+      : "memory");
+}
+// this thread's kTWords words of a parked chunk <-> TMEM
+template <int N>
+__device__ __forceinline__ void tmem_stw(uint32_t taddr, const uint32_t (&r)[N]) {
+  if constexpr (N == 16) tmem_st16(taddr, r);
+  else tmem_st32(taddr, r);
+}
+template <int N>
+__device__ __forceinline__ void tmem_ldw(uint32_t taddr, uint32_t (&r)[N]) {
+  if constexpr (N == 16) tmem_ld16(taddr, r);
+  else tmem_ld32w(taddr, r);
 }
 
-// This thread's share of a chunk as 16 raw 32-bit words (4 x 16-byte vectors).
+// This thread's share of a chunk as kTWords raw 32-bit words (kTV 16-byte vectors).
 // FULL: the chunk is a whole 32 KB (no per-vector bounds checks).
 template <bool FULL = false>
 __device__ __forceinline__ void lds_raw(const uint4* q, int warp, int lane, int nvec,
-                                        uint32_t (&w)[16]) {
+                                        uint32_t (&w)[kTWords]) {
 #pragma unroll
-  for (int j = 0; j < kVecPerThread; ++j) {
-    const int vi = vec_index(warp, lane, j);
+  for (int j = 0; j < kTV; ++j) {
+    const int vi = t_vec_index(warp, lane, j);
     uint4 v = make_uint4(0, 0, 0, 0);
     if (FULL || vi < nvec) v = q[vi];
     w[4 * j + 0] = v.x;
@@ -139,10 +194,10 @@ __device__ __forceinline__ void lds_raw(const uint4* q, int warp, int lane, int 
 }
 template <bool FULL = false>
 __device__ __forceinline__ void sts_raw(uint4* q, int warp, int lane, int nvec,
-                                        const uint32_t (&w)[16]) {
+                                        const uint32_t (&w)[kTWords]) {
 #pragma unroll
-  for (int j = 0; j < kVecPerThread; ++j) {
-    const int vi = vec_index(warp, lane, j);
+  for (int j = 0; j < kTV; ++j) {
+    const int vi = t_vec_index(warp, lane, j);
     if (FULL || vi < nvec)
       q[vi] = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
   }
@@ -158,16 +213,16 @@ template <> struct EFmt<float> { using V = Vec<float>; };
 // Pass-1 fold of one chunk held as raw words: warp-uniform running max, e computed
 // once, the e words returned in place of the logits and the shift c returned.
 template <typename T, bool ENT, bool FULL>
-__device__ __forceinline__ float fold_to_e(RowStat<float>& rs, uint32_t (&w)[16], int warp, int lane,
+__device__ __forceinline__ float fold_to_e(RowStat<float>& rs, uint32_t (&w)[kTWords], int warp, int lane,
                                            int nvec) {
   constexpr int E = Vec<T>::N;
-  constexpr int N = kVecPerThread * E;
+  constexpr int N = kTV * E;
   float f[N];
 #pragma unroll
-  for (int j = 0; j < kVecPerThread; ++j) {
+  for (int j = 0; j < kTV; ++j) {
     float g[E];
     Vec<T>::unpack(make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]), g);
-    const bool ok = FULL || vec_index(warp, lane, j) < nvec;
+    const bool ok = FULL || t_vec_index(warp, lane, j) < nvec;
 #pragma unroll
     for (int e = 0; e < E; ++e) f[j * E + e] = ok ? g[e] : Lim<float>::ninf();
   }
@@ -188,7 +243,7 @@ __device__ __forceinline__ float fold_to_e(RowStat<float>& rs, uint32_t (&w)[16]
   const float2 C2 = make_float2(-c, -c);
   float2 s2 = make_float2(0.f, 0.f), x2 = make_float2(0.f, 0.f);
 #pragma unroll
-  for (int j = 0; j < kVecPerThread; ++j) {
+  for (int j = 0; j < kTV; ++j) {
     float ev[E];
 #pragma unroll
     for (int k = 0; k < E; k += 2) {
@@ -218,9 +273,9 @@ __device__ __forceinline__ float fold_to_e(RowStat<float>& rs, uint32_t (&w)[16]
 // Pass-1 step on one ring chunk: load this thread's words, fold them to e (returns
 // the shift c); full 32 KB chunks take the branch-free path.
 template <typename T, bool ENT>
-__device__ __forceinline__ float chunk_to_e(RowStat<float>& rs, const uint4* q, uint32_t (&wv)[16],
+__device__ __forceinline__ float chunk_to_e(RowStat<float>& rs, const uint4* q, uint32_t (&wv)[kTWords],
                                             int warp, int lane, int nvec) {
-  if ((warp + 1) * (kWarpBytes / 16) <= nvec) {  // this warp's region all valid
+  if ((warp + 1) * (kTWBytes / 16) <= nvec) {  // this warp's region all valid
     lds_raw<true>(q, warp, lane, nvec, wv);
     return fold_to_e<T, ENT, true>(rs, wv, warp, lane, nvec);
   }
@@ -255,14 +310,14 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
   if (tid == 0) {
     for (uint32_t s = 0; s < nslots; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kConsumerWarps);
+      mbar_init(&empty[s], kTW);
     }
     mbar_init(&tail->bcbar[0], 1);
     mbar_init(&tail->bcbar[1], 1);
     for (int j = 0; j < AREAL_N_STATS; ++j) tail->st[j] = 0.0;
     fence_mbar_init_cluster();
   }
-  if (warp == kEpilogueWarp) {  // one warp allocates (and later frees) all of TMEM
+  if (warp == kTEpilogue) {  // one warp allocates (and later frees) all of TMEM
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(&s_tmem_base)),
                  "r"(kTmemCols)
@@ -275,7 +330,7 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
   const uint32_t tbase = s_tmem_base;
   const int64_t cid = blockIdx.x, ncl = gridDim.x;
 
-  if (warp == kProducerWarp) {
+  if (warp == kTProducer) {
     // ================= producer: TMA bulk loads of whole rows, chunk by chunk
     if (lane == 0) {
       Cursor cur = {0u, 0u};
@@ -293,7 +348,7 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
         }
       }
     }
-  } else if (warp == kEpilogueWarp) {
+  } else if (warp == kTEpilogue) {
     // ================= epilogue: merge the 16 partials, fp64 per-token epilogue
     int it = 0;
     for (int64_t row = cid; row < a.n_rows; row += ncl, ++it) {
@@ -310,9 +365,9 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
         sc_adv = a.adv[idx];
         sc_ver = a.versions ? a.versions[idx] : 0;
       }
-      named_bar_sync(kBarPartials, kBarPartialsThreads);
+      named_bar_sync(kBarPartials, kTBarThreads);
       RowStat<A> w;
-      if (lane < kConsumerWarps) {
+      if (lane < kTW) {
         w.m = tail->red[par][lane][0];
         w.s = tail->red[par][lane][1];
         w.sx = tail->red[par][lane][2];
@@ -366,10 +421,10 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
       Cursor cc = cur;
       for (int c = 0; c < la; ++c) {
         const int nvec = (c < nfull ? kChunkBytes : last_bytes) / 16;
-        uint32_t wv[16];
+        uint32_t wv[kTWords];
         lds_raw(reinterpret_cast<const uint4*>(ring + (size_t)cc.slot * kChunkBytes), warp, lane,
                 nvec, wv);
-        tmem_st16(tmem_addr(tbase, warp, c), wv);
+        tmem_stw(tmem_addr(tbase, warp, c), wv);
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[cc.slot]);
         cc.next(nslots);
@@ -380,11 +435,11 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
         mbar_wait(&full[cc.slot], cc.phase);
         const int nvec = (c < nfull ? kChunkBytes : last_bytes) / 16;
         uint4* q = reinterpret_cast<uint4*>(ring + (size_t)cc.slot * kChunkBytes);
-        uint32_t wv[16];
+        uint32_t wv[kTWords];
         const float cshift = chunk_to_e<T, ENT>(rs, q, wv, warp, lane, nvec);
-        if (lane == 0) cw[c * kConsumerWarps + warp] = cshift;
+        if (lane == 0) cw[c * kTW + warp] = cshift;
         if (c < ntm) {
-          tmem_st16(tmem_addr(tbase, warp, c), wv);
+          tmem_stw(tmem_addr(tbase, warp, c), wv);
           __syncwarp();
           if (lane == 0) mbar_arrive(&empty[cc.slot]);
         } else {
@@ -400,7 +455,7 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
         tail->red[par][warp][1] = rs.s;
         tail->red[par][warp][2] = rs.sx;
       }
-      named_bar_arrive(kBarPartials, kBarPartialsThreads);
+      named_bar_arrive(kBarPartials, kTBarThreads);
       // ---- lookahead: fold the next row's first chunks (e in place) during the epilogue
       const bool has_next = row + ncl < a.n_rows;
       const int la_next = has_next ? la_max : 0;
@@ -412,9 +467,9 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
         mbar_wait(&full[lc.slot], lc.phase);
         const int nvec = (c < nfull ? kChunkBytes : last_bytes) / 16;
         uint4* q = reinterpret_cast<uint4*>(ring + (size_t)lc.slot * kChunkBytes);
-        uint32_t wv[16];
+        uint32_t wv[kTWords];
         const float cshift = chunk_to_e<T, ENT>(nxt, q, wv, warp, lane, nvec);
-        if (lane == 0) cwn[c * kConsumerWarps + warp] = cshift;
+        if (lane == 0) cwn[c * kTW + warp] = cshift;
         sts_raw(q, warp, lane, nvec, wv);
         lc.next(nslots);
       }
@@ -449,8 +504,8 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
           const uint4* src = xrow + (size_t)c * (kChunkBytes / 16);
           uint4* dst = reinterpret_cast<uint4*>(drow + (size_t)c * kChunkBytes);
 #pragma unroll
-          for (int j = 0; j < kVecPerThread; ++j) {
-            const int vi = vec_index(warp, lane, j);
+          for (int j = 0; j < kTV; ++j) {
+            const int vi = t_vec_index(warp, lane, j);
             if (vi < nvec) {
               float f[E];
               Vec<T>::unpack(src[vi], f);
@@ -470,10 +525,10 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
       Cursor c2 = cur;
       for (int c = 0; c < nchunks; ++c) {
         const int nvec = (c < nfull ? kChunkBytes : last_bytes) / 16;
-        const bool full = (warp + 1) * (kWarpBytes / 16) <= nvec;  // this warp's region
-        uint32_t wv[16];
+        const bool full = (warp + 1) * (kTWBytes / 16) <= nvec;  // this warp's region
+        uint32_t wv[kTWords];
         if (c < ntm) {
-          tmem_ld16(tmem_addr(tbase, warp, c), wv);
+          tmem_ldw(tmem_addr(tbase, warp, c), wv);
           tmem_wait_ld();
         } else {  // resident tail chunk (its full barrier completed in pass 1)
           const uint4* q = reinterpret_cast<const uint4*>(ring + (size_t)c2.slot * kChunkBytes);
@@ -482,7 +537,7 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
           __syncwarp();
           if (lane == 0) mbar_arrive(&empty[c2.slot]);
         }
-        const float F = g * fast_exp2(cw[c * kConsumerWarps + warp] - lse_s);
+        const float F = g * fast_exp2(cw[c * kTW + warp] - lse_s);
         const float2 F2 = make_float2(F, F);
         uint4* dst = reinterpret_cast<uint4*>(drow + (size_t)c * kChunkBytes);
         // bf16 logits: e is stored as bf16 pairs, so dlogit = e * F is one packed
@@ -497,7 +552,7 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
             o.y = bf162_bits(__hmul2(bits_bf162(wv[4 * j + 1]), Fb));
             o.z = bf162_bits(__hmul2(bits_bf162(wv[4 * j + 2]), Fb));
             o.w = bf162_bits(__hmul2(bits_bf162(wv[4 * j + 3]), Fb));
-            dst[vec_index(warp, lane, j)] = o;
+            dst[t_vec_index(warp, lane, j)] = o;
           } else {
             float f[E];
             EFmt<T>::V::unpack(make_uint4(wv[4 * j], wv[4 * j + 1], wv[4 * j + 2], wv[4 * j + 3]), f);
@@ -507,16 +562,16 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
               f[e] = d.x;
               f[e + 1] = d.y;
             }
-            dst[vec_index(warp, lane, j)] = Vec<T>::pack(f);
+            dst[t_vec_index(warp, lane, j)] = Vec<T>::pack(f);
           }
         };
         if (full) {  // branch-free
 #pragma unroll
-          for (int j = 0; j < kVecPerThread; ++j) scale_store(j);
+          for (int j = 0; j < kTV; ++j) scale_store(j);
         } else {
 #pragma unroll
-          for (int j = 0; j < kVecPerThread; ++j)
-            if (vec_index(warp, lane, j) < nvec) scale_store(j);
+          for (int j = 0; j < kTV; ++j)
+            if (t_vec_index(warp, lane, j) < nvec) scale_store(j);
         }
         c2.next(nslots);
       }
@@ -526,7 +581,7 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
         if (b.tok >= 0 && b.tok < a.vocab) {
           const int ct = (int)(b.tok / per_chunk);
           const int vt = (int)((b.tok - (int64_t)ct * per_chunk) / E);
-          if (warp == vt / (kWarpBytes / 16) && lane == (vt & 31))
+          if (warp == vt / (kTWBytes / 16) && lane == (vt & 31))
             reinterpret_cast<T*>(drow)[b.tok] = dtok;
         }
       }
@@ -535,14 +590,14 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
     tmem_fence_before();
   }
   __syncthreads();
-  if (warp == kEpilogueWarp) {
+  if (warp == kTEpilogue) {
     tmem_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(kTmemCols)
                  : "memory");
   }
   double cta[AREAL_N_STATS];
   for (int j = 0; j < AREAL_N_STATS; ++j) cta[j] = tail->st[j];
-  finalize_stats(a, cta, kRingThreads);
+  finalize_stats(a, cta, kTThreads);
 }
 
 }  // namespace areal
