@@ -191,3 +191,22 @@ def test_linear_ppo_fwd_bwd_row_index_and_prox_from_lp():
     torch.testing.assert_close(outs[0][4][perm.long()], rlp, rtol=0, atol=1e-4)
     s = outs[0][3].cpu().numpy()
     assert s[1] == T and abs(s[3] - T) < 1e-9  # every ratio exactly 1
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_linear_logprob_fuzz(seed):
+    """Seeded random shapes for K7: rows, vocab (tails vs the 256-column tiles and the
+    2048-column blocks), d in multiples of 64, bias on/off, entropy on/off, both CTA
+    groups, fp16/bf16 — against the float64 head + log-softmax."""
+    rng = np.random.default_rng(500 + seed)
+    n = int(rng.integers(1, 700))
+    V = int(rng.integers(1, 20000))
+    d = int(64 * rng.integers(1, 9))
+    dtype = torch.bfloat16 if seed % 2 == 0 else torch.float16
+    h, w, b, tok = _case(n, V, d, dtype=dtype, bias=bool(seed % 3), seed=seed)
+    ent_on = bool(seed % 4 < 2)
+    lp, ent = K.linear_logprob_fwd(h, w, tok, bias=b, with_entropy=ent_on, cta_group=1 + seed % 2)
+    rlp, rent = _ref(h, w, b, tok, entropy=ent_on)
+    torch.testing.assert_close(lp, rlp, rtol=0, atol=ATOL)
+    if ent_on:
+        torch.testing.assert_close(ent, rent, rtol=1e-5, atol=ATOL)
