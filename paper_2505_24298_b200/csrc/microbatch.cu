@@ -61,6 +61,8 @@ __host__ __device__ inline size_t plan_region_a(int n, int npow2) {
   return ((keys > sums ? keys : sums) + 15) & ~(size_t)15;
 }
 
+constexpr int kRegGroups = 128;  // groups whose totals live in warp 0's registers (4 / lane)
+
 __global__ void __launch_bounds__(kPlanThreads) plan_kernel(PlanArgs a, int npow2) {
   extern __shared__ __align__(16) unsigned char sm[];
   const int m = blockIdx.x;
@@ -140,42 +142,75 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(PlanArgs a, int npow
       __syncthreads();
     }
   }
-  // ---- greedy placement (warp 0): Alg. 1
+  // ---- greedy placement (warp 0): Alg. 1.  The loop is one serial chain over the
+  // items (its latency is the kernel's), so it is kept short: the first kRegGroups
+  // groups live in registers, group g on lane g % 32 as room = C - total (-1 while
+  // unopened, so nothing fits) and key = members << 13 | g.  Per item: one compare
+  // + select + min per register group, one REDUX.MIN, a predicated update on the
+  // owner lane.  Groups beyond kRegGroups (tiny items under a large capacity) use
+  // tot / cnt in shared memory.  All sums fit 32 bits: totals <= C < 2^31.
   if (tid < 32) {
+    // four named registers per lane (an array here ends up in local memory)
+    int32_t r0 = -1, r1 = -1, r2 = -1, r3 = -1;
+    uint32_t k0 = lane, k1 = lane + 32, k2 = lane + 64, k3 = lane + 96;
     int G = 0;
-    const int64_t C = a.capacity;
+    const int32_t C = (int32_t)a.capacity;  // validated <= INT32_MAX on the host
     const int kmin = a.min_groups;
+    uint64_t key = n > 0 ? keys[0] : 0;
     for (int p = 0; p < n; ++p) {
-      const uint64_t key = keys[p];
       const int item = (int)(key & 0xffffffffu);
-      const int64_t s = (int64_t)(0xffffffffu - (uint32_t)(key >> 32));
-      uint32_t best = 0xffffffffu;
-      if (G >= kmin) {
-        for (int g = lane; g < G; g += 32) {
-          if ((int64_t)tot[g] + s <= C) {
-            const uint32_t kk = ((uint32_t)cnt[g] << 13) | (uint32_t)g;
-            best = kk < best ? kk : best;
-          }
-        }
-        best = __reduce_min_sync(0xffffffffu, best);
+      const int32_t s = (int32_t)(0xffffffffu - (uint32_t)(key >> 32));
+      if (p + 1 < n) key = keys[p + 1];
+      uint32_t best = s <= r0 ? k0 : 0xffffffffu;
+      best = min(best, s <= r1 ? k1 : 0xffffffffu);
+      best = min(best, s <= r2 ? k2 : 0xffffffffu);
+      best = min(best, s <= r3 ? k3 : 0xffffffffu);
+      for (int g = kRegGroups + lane; g < G; g += 32) {
+        if (s <= C - tot[g]) best = min(best, ((uint32_t)cnt[g] << 13) | (uint32_t)g);
       }
-      if (lane == 0) {
-        int g;
-        if (best == 0xffffffffu) {  // fewer than min_groups, or nothing fits
-          g = G;
+      best = __reduce_min_sync(0xffffffffu, best);
+      // fewer than min_groups, or nothing fits: open group G
+      const bool open = G < kmin || best == 0xffffffffu;
+      const int g = open ? G : (int)(best & 0x1fffu);
+      G += open;
+      if (g < kRegGroups) {
+        if (lane == (g & 31)) {
+          const int j = g >> 5;
+          int32_t room = j == 0 ? r0 : j == 1 ? r1 : j == 2 ? r2 : r3;
+          uint32_t kk = j == 0 ? k0 : j == 1 ? k1 : j == 2 ? k2 : k3;
+          if (open) room = C;
+          gof[item] = g;
+          slt[item] = (int32_t)(kk >> 13);
+          ofs[item] = C - room;
+          room -= s;
+          kk += 1u << 13;
+          r0 = j == 0 ? room : r0; r1 = j == 1 ? room : r1;
+          r2 = j == 2 ? room : r2; r3 = j == 3 ? room : r3;
+          k0 = j == 0 ? kk : k0; k1 = j == 1 ? kk : k1;
+          k2 = j == 2 ? kk : k2; k3 = j == 3 ? kk : k3;
+        }
+      } else if (lane == 0) {
+        if (open) {
           tot[g] = 0;
           cnt[g] = 0;
-        } else {
-          g = (int)(best & 0x1fffu);
         }
         gof[item] = g;
         slt[item] = cnt[g];
         ofs[item] = tot[g];
-        tot[g] += (int32_t)s;
+        tot[g] += s;
         cnt[g] += 1;
       }
-      if (best == 0xffffffffu) ++G;
       __syncwarp();
+    }
+    const int32_t rr[4] = {r0, r1, r2, r3};
+    const uint32_t kq[4] = {k0, k1, k2, k3};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int g = lane + 32 * j;
+      if (g < G) {
+        tot[g] = C - rr[j];
+        cnt[g] = (int32_t)(kq[j] >> 13);
+      }
     }
     if (lane == 0) s_G = G;
   }

@@ -247,6 +247,7 @@ class DecoupledPPOStep:
         self.k1_bytes = 0
         self.k7_flops = 0
         self.record_events = False
+        self._readback = None  # pinned buffer for the plan's host read
 
     # ---- K3
     def advantages(self, ro: PackedRollouts) -> torch.Tensor:
@@ -260,29 +261,54 @@ class DecoupledPPOStep:
 
     # ---- K4 + K5
     def plan(self, ro: PackedRollouts) -> StepPlan:
+        return self._plan_finish(self._plan_launch(ro))
+
+    def _plan_launch(self, ro: PackedRollouts):
+        """Host split + K4, an async read of the plan's sizes into pinned memory, then
+        K5: the host later waits for K4 and that read only (K5 and whatever the caller
+        queues next, e.g. K3, run while it deals the micro-batches)."""
         c = self.cfg
         items = minibatch_items(ro.traj_bounds_host, c.minibatches)
         if not items:
-            return StepPlan(items, None, None, None, None)
+            return items, None
         lens = np.diff(ro.traj_bounds_host)
         mb_offsets = np.concatenate([[0], np.cumsum([len(x) for x in items])]).astype(np.int32)
         mb_tokens = [int(lens[x].sum()) for x in items]
         mb_token_start = np.concatenate([[0], np.cumsum(mb_tokens)[:-1]]).astype(np.int64)
-        flat = torch.from_numpy(np.concatenate(items).astype(np.int32)).to(self.device)
+        flat = np.concatenate(items).astype(np.int32)  # staged with the offsets, one copy
         dplan = K.plan_microbatches(ro.traj_bounds, flat, mb_offsets, mb_token_start,
                                     c.micro_token_budget, c.micro_min_groups)
+        # the single host read of the plan: micro-batch sizes drive the model's shapes
+        M, n_gc = len(items), dplan.group_cu.numel()
+        need = 16 * M + 8 * n_gc
+        if self._readback is None or self._readback.numel() < need:
+            self._readback = torch.empty(max(2 * need, 4096), dtype=torch.uint8).pin_memory()
+        rb = self._readback
+        gcu = rb[:8 * n_gc].view(torch.int64)
+        st = rb[8 * n_gc:8 * n_gc + 4 * M].view(torch.int32)
+        ng = rb[8 * n_gc + 8 * M:8 * n_gc + 12 * M].view(torch.int32)
+        gcu.copy_(dplan.group_cu, non_blocking=True)
+        st.copy_(dplan.status[:M], non_blocking=True)
+        ng.copy_(dplan.n_groups[:M], non_blocking=True)
+        ready = torch.cuda.Event()
+        ready.record()
         gather, _ = K.fill_gather(ro.traj_bounds, dplan, int(sum(mb_tokens)))
         self.launches += 2
-        # the single host sync of the plan: micro-batch sizes drive the model's shapes
-        small = torch.cat([dplan.status[:len(items)].to(torch.int64),
-                           dplan.n_groups[:len(items)].to(torch.int64), dplan.group_cu]).cpu().numpy()
-        M = len(items)
-        status, n_groups, group_cu = small[:M], small[M:2 * M], small[2 * M:]
+        return items, (dplan, gather, mb_offsets, lens, gcu, st, ng, ready)
+
+    def _plan_finish(self, pending) -> StepPlan:
+        items, rest = pending
+        if rest is None:
+            return StepPlan(items, None, None, None, None)
+        dplan, gather, mb_offsets, lens, gcu, st, ng, ready = rest
+        ready.synchronize()
+        status, n_groups, group_cu = st.numpy().copy(), ng.numpy().astype(np.int64), \
+            gcu.numpy().copy()
         bad = np.nonzero(status)[0]
         if len(bad):
             m = int(bad[0])
             raise _status_error(int(status[m]), [int(lens[k]) for k in items[m]],
-                                c.micro_token_budget)
+                                self.cfg.micro_token_budget)
         sp = StepPlan(items, dplan, gather, group_cu, n_groups)
         sp.micro, sp.mine = shard_micro_batches(group_cu, n_groups, mb_offsets, self.world,
                                                 self.rank)
@@ -328,8 +354,11 @@ class DecoupledPPOStep:
     def run(self, ro: PackedRollouts, logits_fn, backward_fn=None, update_fn=None,
             current_version: int = 0, dlogits_fn=None, prox_head_fn=None) -> StepResult:
         c = self.cfg
+        # K4 first: the plan's one host read waits for K4 only; K5 and K3 run
+        # behind it while the host deals the micro-batches and launches the prox pass
+        pending = self._timed(self.k45_events, lambda: self._plan_launch(ro))  # 300-315
         adv = self._timed(self.k3_events, lambda: self.advantages(ro))  # trainer.py:296
-        sp = self._timed(self.k45_events, lambda: self.plan(ro))        # 300-315
+        sp = self._plan_finish(pending)
         decoupled = c.objective == "decoupled"
         M = len(sp.items)
         fuse0 = c.fuse_first_prox and decoupled and M > 0

@@ -22,6 +22,45 @@ ADV_MODES = {"reference": 0, "gae": 1}
 NORMS = {"none": 0, "global": 1, "group": 2, "group_token": 2, "group_sequence": 3}
 
 _WORKSPACES: dict = {}
+_STAGES: dict = {}
+
+
+class _HostStage:
+    """Reusable pinned host buffer for small per-step host->device inputs: several
+    arrays go over in ONE async copy (pageable ``.to(dev)`` copies stage through a
+    driver bounce buffer and block the host).  An event guards reuse until the
+    previous copy has executed."""
+
+    def __init__(self):
+        self.buf = None
+        self.event = None
+
+    def upload(self, arrays, device):
+        offs, n = [], 0
+        for a in arrays:
+            offs.append(n)
+            n += (a.nbytes + 15) // 16 * 16
+        if self.event is not None:
+            self.event.synchronize()
+        if self.buf is None or self.buf.numel() < n:
+            self.buf = torch.empty(max(n, 4096) * 2, dtype=torch.uint8).pin_memory()
+        host = self.buf.numpy()
+        for a, o in zip(arrays, offs):
+            host[o:o + a.nbytes] = a.reshape(-1).view(np.uint8)
+        dev = torch.empty(max(n, 16), dtype=torch.uint8, device=device)
+        dev[:n].copy_(self.buf[:n], non_blocking=True)
+        self.event = torch.cuda.Event()
+        self.event.record()
+        return [dev[o:o + a.nbytes].view(torch.from_numpy(a[:0]).dtype)
+                for a, o in zip(arrays, offs)]
+
+
+def _upload(arrays, device):
+    key = (device.index, torch.cuda.current_stream(device).cuda_stream)
+    st = _STAGES.get(key)
+    if st is None:
+        st = _STAGES[key] = _HostStage()
+    return st.upload([np.ascontiguousarray(a) for a in arrays], device)
 
 
 def _ptr(t):
@@ -213,14 +252,17 @@ def plan_microbatches(traj_bounds: torch.Tensor, item_traj: torch.Tensor, mb_off
                       mb_token_start, capacity: int, min_groups: int) -> DevicePlan:
     """Dynamic micro-batch allocation for every minibatch at once (K4 + packing plan).
 
-    ``item_traj`` (device int32) lists the non-empty trajectories of each
+    ``item_traj`` (device int32, or a host int array: then it travels with the
+    offsets in one pinned async copy) lists the non-empty trajectories of each
     minibatch back to back; ``mb_offsets`` (host, M+1) delimits them;
     ``mb_token_start`` (host, M) is each minibatch's offset in the packed stream.
     """
     lib = _lib.load()
     dev = traj_bounds.device
     _need(traj_bounds, "traj_bounds", torch.int64, dev)
-    _need(item_traj, "item_traj", torch.int32, dev)
+    host_items = not isinstance(item_traj, torch.Tensor)
+    if not host_items:
+        _need(item_traj, "item_traj", torch.int32, dev)
     mb_offsets = np.asarray(mb_offsets, dtype=np.int32)
     mb_token_start = np.asarray(mb_token_start, dtype=np.int64)
     M = len(mb_offsets) - 1
@@ -230,8 +272,13 @@ def plan_microbatches(traj_bounds: torch.Tensor, item_traj: torch.Tensor, mb_off
         raise ValueError(f"{max_items} sequences in one minibatch exceeds "
                          f"{_lib.MAX_ITEMS_PER_MINIBATCH}")
     i32 = dict(dtype=torch.int32, device=dev)
-    mb_off_d = torch.from_numpy(mb_offsets).to(dev, non_blocking=True)
-    mb_tok_d = torch.from_numpy(mb_token_start).to(dev, non_blocking=True)
+    if host_items:  # all three host inputs in one pinned async copy
+        item_traj, mb_off_d, mb_tok_d = _upload(
+            [np.asarray(item_traj, dtype=np.int32), mb_offsets, mb_token_start], dev)
+        if item_traj.numel() < n_items:
+            raise ValueError(f"item_traj has {item_traj.numel()} entries, needs {n_items}")
+    else:
+        mb_off_d, mb_tok_d = _upload([mb_offsets, mb_token_start], dev)
     plan = DevicePlan(
         group_of=torch.empty(n_items, **i32), slot_of=torch.empty(n_items, **i32),
         n_groups=torch.empty(max(M, 1), **i32),
@@ -246,7 +293,7 @@ def plan_microbatches(traj_bounds: torch.Tensor, item_traj: torch.Tensor, mb_off
         _ptr(plan.n_groups), _ptr(plan.group_cu), _ptr(plan.group_seq_cu),
         _ptr(plan.packed_traj), _ptr(plan.seq_cu), _ptr(plan.status), _stream()),
         "areal_plan_microbatches")
-    plan._keepalive = (mb_off_d, mb_tok_d)  # host->device copies are async
+    plan._keepalive = (item_traj, mb_off_d, mb_tok_d)  # host->device copies are async
     return plan
 
 

@@ -410,13 +410,12 @@ def minibatch_items(traj_bounds: np.ndarray, minibatches: int):
     zero-length trajectories (trainer.py:300-301, 310-311)."""
     bounds = np.asarray(traj_bounds, dtype=np.int64)
     n_traj = len(bounds) - 1
+    nonempty = np.diff(bounds) > 0
     out = []
     for mb in np.array_split(np.arange(n_traj), minibatches):
-        if len(mb) == 0:
-            continue
-        ids = [int(k) for k in mb if bounds[k + 1] > bounds[k]]
-        if ids:
-            out.append(ids)
+        ids = mb[nonempty[mb]]
+        if len(ids):
+            out.append(ids.tolist())
     return out
 
 

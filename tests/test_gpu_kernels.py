@@ -337,6 +337,36 @@ def test_allocator_bit_exact_vs_reference_golden():
         assert int(plan.n_groups[0]) == int(c["gid"].max()) + 1
 
 
+def test_plan_host_item_list_matches_device_and_reuses_stage():
+    """item_traj given as a host array (one pinned staged copy) == device item_traj,
+    including back-to-back calls with no sync in between (the staging buffer's reuse
+    waits for the previous copy)."""
+    rng = np.random.default_rng(5)
+    plans = []
+    for trial in range(6):
+        n = int(rng.integers(50, 3000))
+        lengths = rng.integers(1, 80, size=n)
+        bounds = cuda(np.concatenate([[0], np.cumsum(lengths)]).astype(np.int64))
+        order = rng.permutation(n).astype(np.int32)
+        mb = [0, n // 3, n]
+        start = [0, int(lengths[order[:n // 3]].sum())]
+        keep = order.copy()
+        a = K.plan_microbatches(bounds, order, mb, start, 400, 2)
+        order[:] = -1  # the staged copy must already own the data
+        b = K.plan_microbatches(bounds, cuda(keep), mb, start, 400, 2)
+        plans.append((a, b))
+    torch.cuda.synchronize()
+    for a, b in plans:
+        for f in ("group_of", "slot_of", "packed_traj", "seq_cu", "n_groups", "status"):
+            assert torch.equal(getattr(a, f), getattr(b, f)), f
+        assert int(a.status[0]) == 0 and int(a.status[1]) == 0
+        for m in range(2):  # group_cu / group_seq_cu: G + 1 entries per minibatch are set
+            base, G = int(a.mb_offsets[m]) + m, int(a.n_groups[m])
+            for f in ("group_cu", "group_seq_cu"):
+                assert torch.equal(getattr(a, f)[base:base + G + 1],
+                                   getattr(b, f)[base:base + G + 1]), f
+
+
 def test_allocator_errors():
     from paper_2505_24298_b200._lib import ERR_LEN_EXCEEDS_CAPACITY, ERR_LEN_NONPOSITIVE, ArealError
     plan, _ = _plan_one([3, 11, 0], 10, 1)
