@@ -447,7 +447,13 @@ static int launch_ring(PpoArgs a, cudaStream_t stream, int cs_force) {
         return s && atoi(s) == 0;
       }();
       const int64_t row_chunks = (V16 * 16 + kChunkBytes - 1) / kChunkBytes;
-      if (CS > 1 && cs_force == 0 && !tmem_off && row_chunks <= kTmemMaxChunks && nslots == 7)
+      // rows beyond TMEM + the ring stream their middle chunks (ppo_tmem.cuh)
+      static const bool stream_off = [] {
+        const char* s = getenv("AREAL_K2_TMEM_STREAM");
+        return s && atoi(s) == 0;
+      }();
+      if (CS > 1 && cs_force == 0 && !tmem_off && nslots == 7 &&
+          (row_chunks <= kTmemMaxChunks || !stream_off))
         return launch_tmem<T, ENT>(a, stream, d, nslots);
     }
   }

@@ -22,7 +22,14 @@
 // of row i+1's pass 1; resident tail chunks (offset >= kTmemChunks) free their
 // slot in pass 2.  A resident chunk at row offset x is reused by stream
 // position x + nslots, which must not be needed before its row's pass 2 starts:
-// x + nslots > nchunks - 1 + la, i.e. la <= nslots + kTmemChunks - nchunks.
+// x + nslots > nchunks - 1 + la, i.e. la <= nslots - R (R resident chunks).
+//
+// Rows longer than TMEM + the ring (fp32 V = 151,936: 19 chunks) keep at most
+// kTResMax chunks resident (all 7 ring slots by default: 8 in TMEM, 7 resident, 4
+// streamed for that row); the S chunks between the TMEM part and the resident tail
+// are "streamed": folded in pass 1, slot freed at once, and re-read from global
+// memory in pass 2 (recently loaded, mostly from L2), dlogits = g 2^(x log2e - lse).
+// Streamed chunks free their slot in pass 1, so the liveness bound above holds.
 #pragma once
 
 namespace areal {
@@ -79,6 +86,13 @@ constexpr bool kFixedShift = AREAL_K2_FIXED_SHIFT != 0;
 #define AREAL_K2_LA_CAP 3
 #endif
 constexpr int kLookaheadCap = AREAL_K2_LA_CAP;
+// Rows held entirely in TMEM (R = 0: bf16 V <= 131,072, fp32 V <= 65,536) leave the
+// whole ring to the stream, and a longer lookahead pays there: bf16 V = 131,072 at
+// lookahead 3 / 4 / 5: 6.05 / 6.40 / 6.65 TB/s (profiles/r01_k2_lookahead_notail.txt).
+#ifndef AREAL_K2_LA_CAP0
+#define AREAL_K2_LA_CAP0 5
+#endif
+constexpr int kLookaheadCapNoTail = AREAL_K2_LA_CAP0;
 
 #ifndef AREAL_K2_PACKED_BF16_MUL
 #define AREAL_K2_PACKED_BF16_MUL 1
@@ -96,7 +110,33 @@ __device__ __forceinline__ uint32_t bf162_bits(__nv_bfloat162 v) {
   return u;
 }
 constexpr int kTmemCols = 512;
-constexpr int kTmemMaxChunks = 14;    // kTmemChunks + (nslots - 1) with 7 slots
+constexpr int kTmemMaxChunks = 14;    // TMEM + resident chunks: kTmemChunks + (nslots - 1)
+// Resident-tail cap (rows of <= 8 + kTResMax chunks stream nothing).  7 = every ring
+// slot (no lookahead on streaming rows) measured best: fp32 V=151,936 at R = 4 / 5 /
+// 6 / 7: 5.69 / 5.68 / 5.83 / 5.98 TB/s (profiles/r01_k2_streamed_sweep.txt).
+#ifndef AREAL_K2_RES_MAX
+#define AREAL_K2_RES_MAX 7
+#endif
+constexpr int kTResMax = AREAL_K2_RES_MAX;
+// Pass-2 chunk order: 0 = row order; 1 = resident tail, streamed, TMEM; 2 = resident
+// tail, TMEM, streamed.  Writing the resident tail first frees the producer's ring
+// slots early.
+#ifndef AREAL_K2_P2_ORDER
+#define AREAL_K2_P2_ORDER 0
+#endif
+constexpr int kP2Order = AREAL_K2_P2_ORDER;
+// L2 policy for rows with streamed chunks: bit 0 = TMA loads of streamed chunks
+// evict_last (the rest evict_first) so pass 2's re-read hits L2; bit 1 = dlogits
+// stores evict-first (st.global.cs) so they do not push those chunks out.
+#ifndef AREAL_K2_L2_HINTS
+#define AREAL_K2_L2_HINTS 3
+#endif
+constexpr int kL2Hints = AREAL_K2_L2_HINTS;
+template <typename V>
+__device__ __forceinline__ void st_out(V* p, V v, bool stream) {
+  if (stream) __stcs(p, v);
+  else *p = v;
+}
 
 struct TmemTail {
   uint64_t bcbar[2];                          // epilogue -> math warps (row parity)
@@ -283,6 +323,44 @@ __device__ __forceinline__ float chunk_to_e(RowStat<float>& rs, const uint4* q, 
   return fold_to_e<T, ENT, false>(rs, wv, warp, lane, nvec);
 }
 
+// Pass 2 of a streamed chunk: this thread's vectors of chunk c re-read from the
+// logits (last use: evict-first loads; in place safe, each thread reads exactly the
+// vectors it then overwrites), dlogits = g 2^(x log2e - lse).
+template <typename T>
+__device__ __forceinline__ void stream_chunk_dlogits(const PpoArgs& a, int64_t row, char* drow,
+                                                     int c, int nvec, int warp, int lane, float g,
+                                                     float lse_s) {
+  constexpr int E = Vec<T>::N;
+  const uint4* src = reinterpret_cast<const uint4*>(a.logits + row * a.ld_in_bytes) +
+                     (size_t)c * (kChunkBytes / 16);
+  uint4* dst = reinterpret_cast<uint4*>(drow + (size_t)c * kChunkBytes);
+  const float2 L2 = make_float2(Lim<float>::kLog2e, Lim<float>::kLog2e);
+  const float2 C2 = make_float2(-lse_s, -lse_s);
+  const float2 G2 = make_float2(g, g);
+  uint4 v[kTV];
+#pragma unroll
+  for (int j = 0; j < kTV; ++j) {
+    const int vi = t_vec_index(warp, lane, j);
+    v[j] = vi < nvec ? __ldcs(src + vi) : make_uint4(0, 0, 0, 0);
+  }
+#pragma unroll
+  for (int j = 0; j < kTV; ++j) {
+    const int vi = t_vec_index(warp, lane, j);
+    if (vi < nvec) {
+      float f[E];
+      Vec<T>::unpack(v[j], f);
+#pragma unroll
+      for (int e = 0; e < E; e += 2) {
+        const float2 t = ffma2(make_float2(f[e], f[e + 1]), L2, C2);
+        const float2 d = fmul2(make_float2(fast_exp2(t.x), fast_exp2(t.y)), G2);
+        f[e] = d.x;
+        f[e + 1] = d.y;
+      }
+      st_out(&dst[vi], Vec<T>::pack(f), (kL2Hints & 2) != 0);
+    }
+  }
+}
+
 template <typename T, bool ENT>
 __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
   static_assert(sizeof(T) == 2 || sizeof(T) == 4, "TMEM K2 path: 16/32-bit logits");
@@ -301,9 +379,11 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
   const int last_bytes = (int)(row_bytes - (int64_t)nfull * kChunkBytes);
   const int nchunks = nfull + (last_bytes > 0 ? 1 : 0);
   const int ntm = min(nchunks, kTmemChunks);     // chunks parked in TMEM
-  const int R = nchunks - ntm;                   // resident tail chunks
-  const int la_max = min(min(min((int)nslots - R, (int)nslots + kTmemChunks - nchunks), nchunks),
-                         kLookaheadCap);
+  const int R = min(nchunks - ntm, kTResMax);  // resident tail chunks
+  const int S = nchunks - ntm - R;               // streamed chunks [ntm, ntm + S)
+  const int la_max = min(min((int)nslots - R, nchunks), R == 0 ? kLookaheadCapNoTail : kLookaheadCap);
+  // shift slot of chunk c in cw[][]: TMEM chunks, then the resident tail
+  auto cwi = [&](int c) { return c < ntm ? c : c - S; };
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -335,6 +415,7 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
     if (lane == 0) {
       Cursor cur = {0u, 0u};
       uint32_t used = 0;
+      const uint64_t pol_keep = l2_policy_evict_last(), pol_drop = l2_policy_evict_first();
       for (int64_t row = cid; row < a.n_rows; row += ncl) {
         const char* src = a.logits + row * a.ld_in_bytes;
         for (int c = 0; c < nchunks; ++c) {
@@ -342,8 +423,12 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
           else ++used;
           const uint32_t bytes = (uint32_t)(c < nfull ? kChunkBytes : last_bytes);
           mbar_arrive_expect_tx(&full[cur.slot], bytes);
-          bulk_g2s(ring + (size_t)cur.slot * kChunkBytes, src + (size_t)c * kChunkBytes, bytes,
-                   &full[cur.slot]);
+          if ((kL2Hints & 1) && S > 0)
+            bulk_g2s_hint(ring + (size_t)cur.slot * kChunkBytes, src + (size_t)c * kChunkBytes,
+                          bytes, &full[cur.slot], (c >= ntm && c < ntm + S) ? pol_keep : pol_drop);
+          else
+            bulk_g2s(ring + (size_t)cur.slot * kChunkBytes, src + (size_t)c * kChunkBytes, bytes,
+                     &full[cur.slot]);
           cur.next(nslots);
         }
       }
@@ -437,12 +522,16 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
         uint4* q = reinterpret_cast<uint4*>(ring + (size_t)cc.slot * kChunkBytes);
         uint32_t wv[kTWords];
         const float cshift = chunk_to_e<T, ENT>(rs, q, wv, warp, lane, nvec);
-        if (lane == 0) cw[c * kTW + warp] = cshift;
         if (c < ntm) {
+          if (lane == 0) cw[c * kTW + warp] = cshift;
           tmem_stw(tmem_addr(tbase, warp, c), wv);
           __syncwarp();
           if (lane == 0) mbar_arrive(&empty[cc.slot]);
+        } else if (c < ntm + S) {  // streamed: pass 2 re-reads it from global memory
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[cc.slot]);
         } else {
+          if (lane == 0) cw[(c - S) * kTW + warp] = cshift;
           sts_raw(q, warp, lane, nvec, wv);  // resident tail chunk: e in place
         }
         cc.next(nslots);
@@ -497,7 +586,7 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
         Cursor cs = cur;
         for (int c = 0; c < nchunks; ++c) {
           const int nvec = (c < nfull ? kChunkBytes : last_bytes) / 16;
-          if (c >= ntm) {  // resident tail chunk: release its ring slot as usual
+          if (c >= ntm + S) {  // resident tail chunk: release its ring slot as usual
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[cs.slot]);
           }
@@ -522,22 +611,33 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
           cs.next(nslots);
         }
       } else {
-      Cursor c2 = cur;
-      for (int c = 0; c < nchunks; ++c) {
+      const bool st_stream = (kL2Hints & 2) && S > 0;
+      for (int k = 0; k < nchunks; ++k) {
+        // chunk order (kP2Order): row order by default; 1 / 2 put the resident tail
+        // first so its ring slots go back to the producer early (measured no better)
+        const int c = kP2Order == 0 ? k
+                      : k < R ? nchunks - R + k
+                      : kP2Order == 1 ? (k < R + S ? ntm + (k - R) : k - R - S)
+                                      : k - R;
         const int nvec = (c < nfull ? kChunkBytes : last_bytes) / 16;
         const bool full = (warp + 1) * (kTWBytes / 16) <= nvec;  // this warp's region
         uint32_t wv[kTWords];
+        if (c >= ntm && c < ntm + S) {  // streamed chunk: dlogits from the logits
+          stream_chunk_dlogits<T>(a, row, drow, c, nvec, warp, lane, g, lse_s);
+          continue;
+        }
         if (c < ntm) {
           tmem_ldw(tmem_addr(tbase, warp, c), wv);
           tmem_wait_ld();
         } else {  // resident tail chunk (its full barrier completed in pass 1)
-          const uint4* q = reinterpret_cast<const uint4*>(ring + (size_t)c2.slot * kChunkBytes);
+          const uint32_t slot = (cur.slot + (uint32_t)c) % nslots;
+          const uint4* q = reinterpret_cast<const uint4*>(ring + (size_t)slot * kChunkBytes);
           if (full) lds_raw<true>(q, warp, lane, nvec, wv);
           else lds_raw<false>(q, warp, lane, nvec, wv);
           __syncwarp();
-          if (lane == 0) mbar_arrive(&empty[c2.slot]);
+          if (lane == 0) mbar_arrive(&empty[slot]);
         }
-        const float F = g * fast_exp2(cw[c * kTW + warp] - lse_s);
+        const float F = g * fast_exp2(cw[cwi(c) * kTW + warp] - lse_s);
         const float2 F2 = make_float2(F, F);
         uint4* dst = reinterpret_cast<uint4*>(drow + (size_t)c * kChunkBytes);
         // bf16 logits: e is stored as bf16 pairs, so dlogit = e * F is one packed
@@ -552,7 +652,7 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
             o.y = bf162_bits(__hmul2(bits_bf162(wv[4 * j + 1]), Fb));
             o.z = bf162_bits(__hmul2(bits_bf162(wv[4 * j + 2]), Fb));
             o.w = bf162_bits(__hmul2(bits_bf162(wv[4 * j + 3]), Fb));
-            dst[t_vec_index(warp, lane, j)] = o;
+            st_out(&dst[t_vec_index(warp, lane, j)], o, st_stream);
           } else {
             float f[E];
             EFmt<T>::V::unpack(make_uint4(wv[4 * j], wv[4 * j + 1], wv[4 * j + 2], wv[4 * j + 3]), f);
@@ -562,7 +662,7 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
               f[e] = d.x;
               f[e + 1] = d.y;
             }
-            dst[t_vec_index(warp, lane, j)] = Vec<T>::pack(f);
+            st_out(&dst[t_vec_index(warp, lane, j)], Vec<T>::pack(f), st_stream);
           }
         };
         if (full) {  // branch-free
@@ -573,7 +673,6 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
           for (int j = 0; j < kTV; ++j)
             if (t_vec_index(warp, lane, j) < nvec) scale_store(j);
         }
-        c2.next(nslots);
       }
       }  // fast path
       {  // the one-hot element: owner of vector vt of chunk ct

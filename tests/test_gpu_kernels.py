@@ -542,9 +542,9 @@ def test_allocator_max_items_and_limits():
 @pytest.mark.parametrize("dt,V", [("bf16", 262144), ("f32", 151936), ("bf16", 229376),
                                   ("f16", 200003)])
 def test_large_vocab_paths(dt, V):
-    """Rows beyond the TMEM kernel's 14 x 32 KB (bf16 V > 229,376; fp32 V > 114,688)
-    fall back to the cluster-split ring; both sides of the boundary and an odd V
-    match the float64 oracle (K1 and K2)."""
+    """Rows beyond TMEM + the ring (bf16 V > 229,376; fp32 V > 114,688) run the TMEM
+    K2 with streamed middle chunks (re-read in pass 2); both sides of the boundary and
+    an odd V match the float64 oracle (K1 and K2)."""
     T = 12
     logits, x64, tokens, behav, prox, adv = make_case(T, V, dt, seed=V % 97)
     lp, ent = K.logprob_fwd(logits.cuda(), cuda(tokens))
@@ -553,3 +553,34 @@ def test_large_vocab_paths(dt, V):
     dl, st = K.ppo_fwd_bwd(logits.cuda(), cuda(tokens), cuda(behav), cuda(prox), cuda(adv))
     ref = O.surrogate_terms(x64, tokens, behav, prox, adv)
     check_k2(dt, dl.double().cpu().numpy(), st.cpu().numpy(), ref, T)
+
+
+@pytest.mark.parametrize("dt,V", [("f32", 151936), ("bf16", 400000), ("f32", 98304)])
+def test_ppo_tmem_streamed_chunks(dt, V):
+    """TMEM K2 on rows with streamed chunks (fp32 V = 151,936: 8 in TMEM, 7 resident,
+    4 streamed): entropy + lp outputs, in-place dlogits, the one-hot element inside a
+    streamed chunk, and an overflow row (fixed-shift slow path) against the oracle."""
+    T = 40
+    logits, x64, tokens, behav, prox, adv = make_case(T, V, dt, seed=V % 89)
+    es = 4 if dt == "f32" else 2
+    mid = (8 * 32768 + 1000) // es            # inside the first streamed chunk
+    tokens[0] = min(mid, V - 1)
+    tokens[1] = min(mid + 40000 // es, V - 1)
+    lg = logits.clone()
+    lg[2, : V // 3] = -50.0                   # later spike above the fixed shift
+    lg[2, V // 2: V // 2 + 5] = 70.0
+    x64 = lg.double().numpy()
+    lp_ref = O.token_logprobs(x64, tokens)
+    prox = lp_ref + 0.02
+    behav = prox + 0.1
+    ref = O.surrogate_terms(x64, tokens, behav, prox, adv)
+    lp = torch.zeros(T, dtype=torch.float64, device="cuda")
+    ent = torch.zeros(T, dtype=torch.float64, device="cuda")
+    g = lg.cuda()
+    dl, st = K.ppo_fwd_bwd(g, cuda(tokens), cuda(behav), cuda(prox), cuda(adv), dlogits=g,
+                           lp_out=lp, entropy_out=ent)          # in place
+    assert dl.data_ptr() == g.data_ptr()
+    check_k2(dt, dl.double().cpu().numpy(), st.cpu().numpy(), ref, T)
+    ok, err = rel_close(lp.cpu().numpy(), lp_ref, TOL[dt])
+    assert ok, err
+    assert np.allclose(ent.cpu().numpy(), O.token_entropy(x64), rtol=TOL[dt], atol=TOL[dt] * 10)
