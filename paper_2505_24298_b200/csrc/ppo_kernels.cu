@@ -452,7 +452,12 @@ static int launch_ring(PpoArgs a, cudaStream_t stream, int cs_force) {
         const char* s = getenv("AREAL_K2_TMEM_STREAM");
         return s && atoi(s) == 0;
       }();
-      if (CS > 1 && cs_force == 0 && !tmem_off && nslots == 7 &&
+      // 16-bit rows that fit the ring also run faster on the TMEM kernel (e-form
+      // pass 2, longer lookahead): bf16 V = 32,000 5.83 -> 6.51 TB/s, V = 65,536
+      // 5.95 -> 6.65; fp32 rows that fit stay on the ring (V = 32,000: 6.67 vs 6.39)
+      // (profiles/r01_k2_small_rows_tmem.txt)
+      const bool small_ok = sizeof(T) == 2;
+      if ((CS > 1 || small_ok) && cs_force == 0 && !tmem_off && nslots == 7 &&
           (row_chunks <= kTmemMaxChunks || !stream_off))
         return launch_tmem<T, ENT>(a, stream, d, nslots);
     }
