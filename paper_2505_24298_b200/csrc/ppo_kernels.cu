@@ -335,6 +335,231 @@ __device__ __forceinline__ void row_warp_body(const PpoArgs& a) {
 
 namespace areal {
 
+// ================================================================== row_cta kernel
+// Rows whose byte length or start is not 16-byte aligned (e.g. bf16 V = 50,257: the
+// 1-D bulk copies of the ring / TMEM kernels need 16-byte granules).  One 512-thread
+// CTA per row, 2 CTAs per SM, so the rows in flight (~300 x 100 KB) stay in L2 and
+// pass 2's re-read does not go back to HBM.  Each row is split into a scalar head up
+// to the first 16-byte boundary, a 16-byte-vector body and a scalar tail; dlogits use
+// vector stores when their row has the same 16-byte phase as the logits row.
+// K1 (read-only) wants many rows in flight to hide each row's serial epilogue: 8 x 256
+// threads per SM; K2 re-reads each row in pass 2 and wants it still in L2: 2 x 512
+// (profiles/r01_rowcta_sweep.txt).
+template <bool BWD> struct RowCtaGeo {
+  static constexpr int kThreads = BWD ? 512 : 256;
+  static constexpr int kBlocks = BWD ? 2 : 8;  // CTAs per SM
+};
+constexpr int kRowCtaUnroll = 4;
+
+template <typename T>
+struct RowSplit {
+  int64_t nh, nv, V;  // head elements, body vectors, row length
+  __device__ __forceinline__ RowSplit(const char* x, int64_t V_) : V(V_) {
+    const int hb = (int)((16 - ((uintptr_t)x & 15)) & 15);
+    nh = hb / (int)sizeof(T);
+    if (nh > V) nh = V;
+    nv = (V - nh) / Vec<T>::N;
+  }
+  __device__ __forceinline__ int64_t tail0() const { return nh + nv * Vec<T>::N; }
+};
+
+// Per-thread running (m, s, sx) over E values at a time.  fp32: the shift moves only
+// when a vector raises the thread's max (rare after the first few), so most vectors
+// are FFMA2 + 2 MUFU ex2 + FADD2 per pair; fp64: the generic fold.
+template <typename A, bool ENT, int E>
+__device__ __forceinline__ void rowcta_fold(RowStat<A>& rs, const A (&f)[E]) {
+  A lmax = f[0];
+#pragma unroll
+  for (int e = 1; e < E; ++e) lmax = fmax(lmax, f[e]);
+  if constexpr (std::is_same<A, float>::value && E % 2 == 0) {
+    if (lmax > rs.m) {
+      const float r = rs.m == Lim<float>::ninf() ? 0.f : fast_exp2((rs.m - lmax) * Lim<float>::kLog2e);
+      rs.s *= r;
+      if (ENT) rs.sx *= r;
+      rs.m = lmax;
+    }
+    if (rs.m == Lim<float>::ninf()) return;  // only -inf so far: contributes nothing
+    const float c = rs.m * Lim<float>::kLog2e;
+    const float2 L2 = make_float2(Lim<float>::kLog2e, Lim<float>::kLog2e);
+    const float2 C2 = make_float2(-c, -c);
+    float2 s2 = make_float2(0.f, 0.f), x2 = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int e = 0; e < E; e += 2) {
+      const float2 v = make_float2(f[e], f[e + 1]);
+      const float2 t = ffma2(v, L2, C2);
+      const float2 ee = make_float2(fast_exp2(t.x), fast_exp2(t.y));
+      s2 = fadd2(s2, ee);
+      if (ENT)
+        x2 = ffma2(ee, make_float2(fmaxf(v.x, Lim<float>::lowest()), fmaxf(v.y, Lim<float>::lowest())), x2);
+    }
+    rs.s += s2.x + s2.y;
+    if (ENT) rs.sx += x2.x + x2.y;
+  } else {
+    fold(rs, f, lmax);
+  }
+}
+
+template <typename T, bool BWD, bool ENT>
+__device__ __forceinline__ void row_cta_body(const PpoArgs& a) {
+  constexpr int kRowCtaThreads = RowCtaGeo<BWD>::kThreads;
+  using A = typename Traits<T>::Acc;
+  constexpr int E = Vec<T>::N;
+  using U = typename std::conditional<std::is_same<T, double>::value, double, float>::type;
+  constexpr int NW = kRowCtaThreads / 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ A red[NW][3];
+  __shared__ double bc[4];  // g, lse_s, token, token's dlogit
+  double st[AREAL_N_STATS];
+#pragma unroll
+  for (int j = 0; j < AREAL_N_STATS; ++j) st[j] = 0.0;
+  const int64_t V = a.vocab;
+  for (int64_t row = blockIdx.x; row < a.n_rows; row += gridDim.x) {
+    const char* xb = a.logits + row * a.ld_in_bytes;
+    const T* x = reinterpret_cast<const T*>(xb);
+    const RowSplit<T> sp(xb, V);
+    const uint4* xv = reinterpret_cast<const uint4*>(x + sp.nh);
+    const int64_t t0 = sp.tail0();
+    const int64_t n_edge = sp.nh + (V - t0);
+    RowStat<A> rs;
+    rs.init();
+    // ---- pass 1: head / tail scalars, then the vector body kRowCtaUnroll deep
+    for (int64_t i = tid; i < n_edge; i += kRowCtaThreads) {
+      const int64_t k = i < sp.nh ? i : t0 + (i - sp.nh);
+      const A v[1] = {Traits<T>::to_acc(x[k])};
+      fold(rs, v, v[0]);
+    }
+    for (int64_t i0 = tid; i0 < sp.nv; i0 += kRowCtaThreads * kRowCtaUnroll) {
+      uint4 q[kRowCtaUnroll];
+#pragma unroll
+      for (int u = 0; u < kRowCtaUnroll; ++u) {
+        const int64_t i = i0 + (int64_t)u * kRowCtaThreads;
+        q[u] = i < sp.nv ? xv[i] : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < kRowCtaUnroll; ++u) {
+        if (i0 + (int64_t)u * kRowCtaThreads < sp.nv) {
+          U g[E];
+          Vec<T>::unpack(q[u], g);
+          A f[E];
+#pragma unroll
+          for (int e = 0; e < E; ++e) f[e] = (A)g[e];
+          rowcta_fold<A, ENT, E>(rs, f);
+        }
+      }
+    }
+    rs.warp_reduce();
+    if (lane == 0) {
+      red[warp][0] = rs.m;
+      red[warp][1] = rs.s;
+      red[warp][2] = rs.sx;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      RowStat<A> w;
+      if (lane < NW) {
+        w.m = red[lane][0];
+        w.s = red[lane][1];
+        w.sx = red[lane][2];
+      } else {
+        w.init();
+      }
+      w.warp_reduce();
+      if (lane == 0) {
+        const A lse_s = Ex<A>::lse_shift(w.m == Lim<A>::ninf() ? A(0) : w.m, w.s);
+        const double lse = Ex<A>::lse_nat(lse_s);
+        const double ent = ENT ? lse - (double)(w.sx / w.s) : 0.0;
+        const int64_t idx = a.row_index ? (int64_t)a.row_index[row] : row;
+        const int64_t tok = a.tokens[idx];
+        const double xt = token_logit<T>(a, x, tok);
+        const double lp = xt - lse;
+        if (a.lp_out) a.lp_out[idx] = lp;
+        if (ENT && a.ent_out) a.ent_out[idx] = ent;
+        if (BWD) {
+          const double prox = a.prox_from_lp ? lp : (a.prox ? a.prox[idx] : 0.0);
+          const TokenTerms t = ppo_token(lp, a.behav[idx], prox, a.adv[idx],
+                                         a.versions ? a.versions[idx] : 0, a);
+          stats_add(st, t, ENT ? ent : 0.0);
+          const double gc = a.grad_scale * t.coef;
+          bc[0] = gc;
+          bc[1] = (double)lse_s;
+          bc[2] = (double)tok;
+          bc[3] = gc * (exp(lp) - 1.0);
+        }
+      }
+    }
+    __syncthreads();
+    if (BWD) {
+      // ---- pass 2 (re-read from L2): dlogits = g * softmax; the one-hot element is
+      // patched after a barrier by thread 0 (the barrier orders the two stores)
+      const A g = (A)bc[0];
+      const A lse_s = (A)bc[1];
+      char* db = a.dlogits + row * a.ld_out_bytes;
+      T* d = reinterpret_cast<T*>(db);
+      auto dsm = [&](A xv_) {
+        if constexpr (std::is_same<A, float>::value)
+          return g * fast_exp2(fmaf(xv_, Lim<float>::kLog2e, -lse_s));
+        else
+          return g * exp(xv_ - lse_s);
+      };
+      for (int64_t i = tid; i < n_edge; i += kRowCtaThreads) {
+        const int64_t k = i < sp.nh ? i : t0 + (i - sp.nh);
+        d[k] = Traits<T>::from_acc(dsm(Traits<T>::to_acc(x[k])));
+      }
+      const bool vec_out = (((uintptr_t)db ^ (uintptr_t)xb) & 15) == 0;
+      uint4* dv = reinterpret_cast<uint4*>(d + sp.nh);
+      for (int64_t i0 = tid; i0 < sp.nv; i0 += kRowCtaThreads * kRowCtaUnroll) {
+        uint4 q[kRowCtaUnroll];
+#pragma unroll
+        for (int u = 0; u < kRowCtaUnroll; ++u) {
+          const int64_t i = i0 + (int64_t)u * kRowCtaThreads;
+          q[u] = i < sp.nv ? __ldcs(xv + i) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < kRowCtaUnroll; ++u) {
+          const int64_t i = i0 + (int64_t)u * kRowCtaThreads;
+          if (i < sp.nv) {
+            U gg[E];
+            Vec<T>::unpack(q[u], gg);
+#pragma unroll
+            for (int e = 0; e < E; ++e) gg[e] = (U)dsm((A)gg[e]);
+            if (vec_out) {
+              __stcs(dv + i, Vec<T>::pack(gg));
+            } else {
+              const int64_t k0 = sp.nh + i * E;
+#pragma unroll
+              for (int e = 0; e < E; ++e) d[k0 + e] = Traits<T>::from_acc((A)gg[e]);
+            }
+          }
+        }
+      }
+      __syncthreads();
+      const int64_t tok = (int64_t)bc[2];
+      if (tid == 0 && tok >= 0 && tok < V) d[tok] = Traits<T>::from_acc((A)bc[3]);
+    }
+  }
+  if (BWD) {
+    __shared__ double cst[AREAL_N_STATS];
+    if (tid == 0)
+      for (int j = 0; j < AREAL_N_STATS; ++j) cst[j] = st[j];
+    __syncthreads();
+    double cta[AREAL_N_STATS];
+    for (int j = 0; j < AREAL_N_STATS; ++j) cta[j] = cst[j];
+    finalize_stats(a, cta, kRowCtaThreads);
+  }
+}
+
+template <typename T, bool ENT>
+__global__ void __launch_bounds__(RowCtaGeo<false>::kThreads, RowCtaGeo<false>::kBlocks)
+    logprob_rowcta_kernel(PpoArgs a) {
+  row_cta_body<T, false, ENT>(a);
+}
+template <typename T, bool ENT>
+__global__ void __launch_bounds__(RowCtaGeo<true>::kThreads, RowCtaGeo<true>::kBlocks)
+    ppo_rowcta_kernel(PpoArgs a) {
+  row_cta_body<T, true, ENT>(a);
+}
+
+
 template <typename T, bool ENT>
 __global__ void __launch_bounds__(kTThreads, 1) ppo_tmem_kernel(PpoArgs a) {
   if constexpr (sizeof(T) == 2 || sizeof(T) == 4) tmem_k2_body<T, ENT>(a);
@@ -512,6 +737,17 @@ static int launch_warp(PpoArgs a, cudaStream_t stream) {
   return AREAL_OK;
 }
 
+template <typename T, bool BWD>
+static int launch_rowcta(PpoArgs a, cudaStream_t stream) {
+  DevInfo d = get_dev();
+  const int64_t grid = std::min<int64_t>(a.n_rows, (int64_t)d.sms * RowCtaGeo<BWD>::kBlocks);
+  auto kern = a.ent_out ? (BWD ? ppo_rowcta_kernel<T, true> : logprob_rowcta_kernel<T, true>)
+                        : (BWD ? ppo_rowcta_kernel<T, false> : logprob_rowcta_kernel<T, false>);
+  kern<<<(unsigned)grid, RowCtaGeo<BWD>::kThreads, 0, stream>>>(a);
+  AREAL_CUDA_CHECK_LAUNCH();
+  return AREAL_OK;
+}
+
 static int dtype_size(int dtype) {
   switch (dtype) {
     case AREAL_F32: return 4;
@@ -525,6 +761,14 @@ static int dtype_size(int dtype) {
 // AUTO: ring when rows are >= 16 KB and every row start is 16-byte aligned.
 static bool ring_ok(const void* base, int64_t ld_bytes, int64_t vocab, int es) {
   return ((uintptr_t)base % 16 == 0) && (ld_bytes % 16 == 0) && ((vocab * es) % 16 == 0);
+}
+
+static bool rowcta_off() {  // AREAL_ROWCTA=0: unaligned rows on the one-warp kernel
+  static const bool off = [] {
+    const char* s = getenv("AREAL_ROWCTA");
+    return s && atoi(s) == 0;
+  }();
+  return off;
 }
 
 template <bool BWD>
@@ -550,6 +794,16 @@ static int dispatch(PpoArgs a, int dtype, int algo, cudaStream_t stream) {
       default: return AREAL_ERR_BAD_DTYPE;
     }
     if (rc != AREAL_ERR_UNSUPPORTED || algo == AREAL_ALGO_ROW_RING) return rc;
+  }
+  // unaligned (or ring-refused) rows of >= 16 KB: one CTA per row, body in 16-byte vectors
+  if (algo == AREAL_ALGO_AUTO && a.vocab * es >= 16384 && !rowcta_off()) {
+    switch (dtype) {
+      case AREAL_F32: return launch_rowcta<float, BWD>(a, stream);
+      case AREAL_BF16: return launch_rowcta<__nv_bfloat16, BWD>(a, stream);
+      case AREAL_F16: return launch_rowcta<__half, BWD>(a, stream);
+      case AREAL_F64: return launch_rowcta<double, BWD>(a, stream);
+      default: return AREAL_ERR_BAD_DTYPE;
+    }
   }
   switch (dtype) {
     case AREAL_F32: return launch_warp<float, BWD>(a, stream);

@@ -584,3 +584,35 @@ def test_ppo_tmem_streamed_chunks(dt, V):
     ok, err = rel_close(lp.cpu().numpy(), lp_ref, TOL[dt])
     assert ok, err
     assert np.allclose(ent.cpu().numpy(), O.token_entropy(x64), rtol=TOL[dt], atol=TOL[dt] * 10)
+
+
+@pytest.mark.parametrize("dt,V", [("bf16", 50257), ("f32", 50257), ("f16", 100003), ("f64", 4097)])
+def test_unaligned_rows_cta_kernel(dt, V):
+    """Rows whose length in bytes is not a multiple of 16 (GPT-2's V = 50,257) run the
+    one-CTA-per-row kernel (scalar head / 16-byte body / scalar tail per row, every row
+    at a different 16-byte phase): K1 lp + entropy and K2 (with row_index gather and a
+    dlogits buffer at a different phase from the logits) match the float64 oracle."""
+    T = 48
+    logits, x64, tokens, behav, prox, adv = make_case(T, V, dt, seed=V % 71)
+    tokens[0], tokens[1], tokens[2] = 0, V - 1, 3     # head / tail elements
+    lp_ref = O.token_logprobs(x64, tokens)
+    lp, ent = K.logprob_fwd(logits.cuda(), cuda(tokens))
+    ok, err = rel_close(lp.cpu().numpy(), lp_ref, TOL[dt])
+    assert ok, err
+    assert np.allclose(ent.cpu().numpy(), O.token_entropy(x64), rtol=TOL[dt], atol=TOL[dt] * 10)
+    ref = O.surrogate_terms(x64, tokens, behav, prox, adv)
+    # packed rows in reverse order through row_index; dlogits rows at another phase
+    order = np.arange(T)[::-1].copy()
+    lg = logits[torch.from_numpy(order)].cuda()
+    big = torch.zeros(T, V + 1, dtype=lg.dtype, device="cuda")
+    dl_view = big[:, 1:]
+    dl, st = K.ppo_fwd_bwd(lg, cuda(tokens), cuda(behav), cuda(prox), cuda(adv),
+                           row_index=cuda(order.astype(np.int32)), dlogits=dl_view)
+    got = np.empty((T, V))
+    got[order] = dl.double().cpu().numpy()
+    check_k2(dt, got, st.cpu().numpy(), ref, T)
+    assert torch.all(big[:, 0] == 0)                  # nothing written outside the rows
+    # in place
+    g = logits.cuda()
+    dl2, st2 = K.ppo_fwd_bwd(g, cuda(tokens), cuda(behav), cuda(prox), cuda(adv), dlogits=g)
+    check_k2(dt, dl2.double().cpu().numpy(), st2.cpu().numpy(), ref, T)

@@ -13,7 +13,7 @@ ap.add_argument("--iters", type=int, default=10)
 ap.add_argument("--algo", default="auto")
 ap.add_argument("--which", default="k1,k2")
 a = ap.parse_args()
-dt = {"bf16": torch.bfloat16, "f32": torch.float32, "f16": torch.float16}[a.dtype]
+dt = {"bf16": torch.bfloat16, "f32": torch.float32, "f16": torch.float16, "f64": torch.float64}[a.dtype]
 dev = torch.device("cuda", 0)
 T, V = a.rows, a.vocab
 x = torch.empty(T, V, dtype=dt, device=dev).normal_(0, 2)
