@@ -59,11 +59,13 @@ typedef enum {
 
 typedef enum { AREAL_F32 = 0, AREAL_BF16 = 1, AREAL_F16 = 2, AREAL_F64 = 3 } areal_dtype_t;
 
-/* Kernel selection for K1/K2.  AUTO picks, for 16-byte-aligned rows: K2 on rows
- * larger than one CTA's shared memory -> the Tensor-Memory kernel (row parked in
- * TMEM, up to 14 x 32 KB), beyond that a thread-block-cluster split of ROW_RING;
- * smaller rows and all of K1 -> ROW_RING (TMA bulk ring); rows under 16 KB or
- * unaligned -> ROW_WARP (one warp per row). */
+/* Kernel selection for K1/K2.  AUTO picks, for 16-byte-aligned rows of >= 16 KB:
+ * K2 on 16-bit rows and on fp32 rows larger than one CTA's shared memory -> the
+ * Tensor-Memory kernel (8 x 32 KB parked in TMEM, up to 7 resident in the ring, the
+ * rest streamed); other K2 rows (fp32 / fp64 that fit, fp64 beyond via a cluster
+ * split) and all of K1 -> ROW_RING (TMA bulk ring).  Unaligned rows of >= 16 KB ->
+ * one CTA per row; rows under 16 KB -> ROW_WARP (one warp per row).  ROW_RING /
+ * ROW_WARP force the respective family. */
 typedef enum { AREAL_ALGO_AUTO = 0, AREAL_ALGO_ROW_WARP = 1, AREAL_ALGO_ROW_RING = 2 } areal_algo_t;
 
 /* Order of the float64 statistics vector (accumulated with +=). */

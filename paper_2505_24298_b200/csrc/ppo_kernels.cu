@@ -7,17 +7,21 @@
 //
 // Kernels (AREAL_ALGO_AUTO picks per shape):
 //   row_warp : one warp per row, any vocab / alignment; both passes read global
-//              memory (the second pass hits L1/L2).  Rows under 16 KB or unaligned.
+//              memory (the second pass hits L1/L2).  Rows under 16 KB.
+//   row_cta  : one CTA per row for rows >= 16 KB that are not 16-byte aligned
+//              (scalar head / 16-byte-vector body / scalar tail; K2 re-reads from L2).
 //   row_ring : persistent, warp-specialised (ppo_ring.cuh).  A producer thread
 //              streams each row through a ring of 32 KB shared-memory chunks with
 //              1-D TMA bulk copies (cp.async.bulk + mbarrier complete_tx).  K1 frees
-//              a chunk as soon as it is in registers; K2 keeps the row resident, and
-//              rows larger than the ring are split over a thread-block cluster whose
-//              CTAs exchange their partials through DSMEM; pass 2 rewrites each chunk
-//              in place as dlogits and bulk-stores it.
-//   tmem     : K2 for rows larger than one CTA's shared memory (ppo_tmem.cuh): the
-//              row's first 8 chunks are parked in Tensor Memory as e = 2^(x - c),
-//              the tail stays in the ring, one CTA per row (the bf16 V ~ 152K default).
+//              a chunk as soon as it is in registers (all aligned K1 rows >= 16 KB);
+//              K2 (fp32 / fp64 rows that fit) keeps the row resident, and rows larger
+//              than the ring are split over a thread-block cluster whose CTAs exchange
+//              their partials through DSMEM; pass 2 rewrites each chunk in place.
+//   tmem     : K2 for all aligned 16-bit rows and fp32 rows beyond the ring
+//              (ppo_tmem.cuh): the row's first 8 chunks are parked in Tensor Memory as
+//              e = 2^(x - c), up to 7 more stay resident in the ring, any further
+//              middle chunks are streamed and re-read from L2 in pass 2; one CTA per
+//              row (the bf16 V ~ 152K default).
 // HBM traffic = one logits read (+ one dlogits write for K2) per element.
 #include <cstdlib>
 #include <type_traits>
