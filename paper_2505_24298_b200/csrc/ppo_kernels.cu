@@ -564,9 +564,9 @@ __global__ void __launch_bounds__(RowCtaGeo<true>::kThreads, RowCtaGeo<true>::kB
 }
 
 
-template <typename T, bool ENT>
+template <typename T, bool ENT, bool UNAL>
 __global__ void __launch_bounds__(kTThreads, 1) ppo_tmem_kernel(PpoArgs a) {
-  if constexpr (sizeof(T) == 2 || sizeof(T) == 4) tmem_k2_body<T, ENT>(a);
+  if constexpr (sizeof(T) == 2 || sizeof(T) == 4) tmem_k2_body<T, ENT, UNAL>(a);
 }
 
 // Distinct entry points per op so profiles name them: K1 = logprob_*, K2 = ppo_*.
@@ -618,14 +618,15 @@ static size_t tmem_smem_bytes(int nslots) {
   return (size_t)nslots * kChunkBytes + 2 * (size_t)nslots * sizeof(uint64_t) + sizeof(TmemTail);
 }
 
-template <typename T, bool ENT>
+template <typename T, bool ENT, bool UNAL = false>
 static int launch_tmem(PpoArgs a, cudaStream_t stream, const DevInfo& d, int nslots) {
+  if (a.vocab >= (int64_t)1 << 30) return AREAL_ERR_UNSUPPORTED;  // 32-bit element indices
   a.cluster_size = 1;
   a.slice16 = (a.vocab * (int64_t)sizeof(T)) / 16;
   a.nslots = nslots;
   const size_t smem = tmem_smem_bytes(nslots);
   if (smem + 256 > (size_t)d.smem_optin) return AREAL_ERR_UNSUPPORTED;  // + static smem
-  auto kern = ppo_tmem_kernel<T, ENT>;
+  auto kern = ppo_tmem_kernel<T, ENT, UNAL>;
   static thread_local int attr_set[16] = {0};
   const int dev = d.dev & 15;
   if (!attr_set[dev]) {
@@ -767,6 +768,20 @@ static bool ring_ok(const void* base, int64_t ld_bytes, int64_t vocab, int es) {
   return ((uintptr_t)base % 16 == 0) && (ld_bytes % 16 == 0) && ((vocab * es) % 16 == 0);
 }
 
+static bool tmem_unaligned_ok(const PpoArgs& a, int es) {
+  static const bool off = [] {  // AREAL_K2_TMEM_UNALIGNED=0: unaligned rows on the row-CTA kernel
+    const char* s = getenv("AREAL_K2_TMEM_UNALIGNED");
+    return s && atoi(s) == 0;
+  }();
+  if (off || a.dlogits == nullptr) return false;
+  const int64_t rb = a.vocab * es;
+  if (rb < 16384) return false;
+  if ((((uintptr_t)a.dlogits - (uintptr_t)a.logits) & 15) != 0) return false;
+  if (((a.ld_out_bytes - a.ld_in_bytes) & 15) != 0) return false;
+  const int64_t lo = (rb + 15) & ~(int64_t)15, hi = (rb + 16 - es + 15) & ~(int64_t)15;
+  return (lo + kChunkBytes - 1) / kChunkBytes == (hi + kChunkBytes - 1) / kChunkBytes;
+}
+
 static bool rowcta_off() {  // AREAL_ROWCTA=0: unaligned rows on the one-warp kernel
   static const bool off = [] {
     const char* s = getenv("AREAL_ROWCTA");
@@ -798,6 +813,24 @@ static int dispatch(PpoArgs a, int dtype, int algo, cudaStream_t stream) {
       default: return AREAL_ERR_BAD_DTYPE;
     }
     if (rc != AREAL_ERR_UNSUPPORTED || algo == AREAL_ALGO_ROW_RING) return rc;
+  }
+  // unaligned K2 rows of >= 16 KB on the TMEM kernel: each row is loaded from the
+  // 16-byte boundary below it (masked head / tail elements); needs dlogits rows at the
+  // same 16-byte phase and a chunk count that the head bytes never change
+  if (BWD && !aligned && algo == AREAL_ALGO_AUTO && (es == 2 || es == 4) && tmem_unaligned_ok(a, es)) {
+    DevInfo d = get_dev();
+    const int nslots = max_slots(d);
+    if (nslots == 7) {
+      const bool ent = a.ent_out != nullptr;
+      int rc = AREAL_ERR_UNSUPPORTED;
+      switch (dtype) {
+        case AREAL_F32: rc = ent ? launch_tmem<float, true, true>(a, stream, d, nslots) : launch_tmem<float, false, true>(a, stream, d, nslots); break;
+        case AREAL_BF16: rc = ent ? launch_tmem<__nv_bfloat16, true, true>(a, stream, d, nslots) : launch_tmem<__nv_bfloat16, false, true>(a, stream, d, nslots); break;
+        case AREAL_F16: rc = ent ? launch_tmem<__half, true, true>(a, stream, d, nslots) : launch_tmem<__half, false, true>(a, stream, d, nslots); break;
+        default: break;
+      }
+      if (rc != AREAL_ERR_UNSUPPORTED) return rc;
+    }
   }
   // unaligned (or ring-refused) rows of >= 16 KB: one CTA per row, body in 16-byte vectors
   if (algo == AREAL_ALGO_AUTO && a.vocab * es >= 16384 && !rowcta_off()) {

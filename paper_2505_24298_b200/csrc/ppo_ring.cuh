@@ -167,6 +167,46 @@ __device__ __noinline__ RowStat<float> row_stats_global(const PpoArgs& a, int64_
   return r;
 }
 
+// The same for a row that starts hb bytes past the 16-byte boundary the vectors are
+// read from (TMEM K2 on unaligned rows): elements outside the row are skipped.
+template <typename T, bool ENT>
+__device__ __noinline__ RowStat<float> row_stats_masked(const PpoArgs& a, int64_t row, int hb,
+                                                        int lane) {
+  constexpr int E = Vec<T>::N;
+  const uint4* q = reinterpret_cast<const uint4*>(a.logits + row * a.ld_in_bytes - hb);
+  const int64_t lo = hb / (int)sizeof(T), hi = lo + a.vocab;  // row = stream elements [lo, hi)
+  const int64_t nv = (hb + a.vocab * (int64_t)sizeof(T) + 15) / 16;
+  float m = Lim<float>::ninf();
+  for (int64_t i = lane; i < nv; i += 32) {
+    float f[E];
+    Vec<T>::unpack(q[i], f);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const bool in = i * E + e >= lo && i * E + e < hi;
+      m = in ? fmaxf(m, f[e]) : m;
+    }
+  }
+  m = warp_max(m);
+  const float c = (m == Lim<float>::ninf()) ? 0.f : m * Lim<float>::kLog2e;
+  float s = 0.f, sx = 0.f;
+  for (int64_t i = lane; i < nv; i += 32) {
+    float f[E];
+    Vec<T>::unpack(q[i], f);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const bool in = i * E + e >= lo && i * E + e < hi;
+      const float ee = in ? fast_exp2(fmaf(f[e], Lim<float>::kLog2e, -c)) : 0.f;
+      s += ee;
+      if (ENT) sx = in ? fmaf(ee, fmaxf(f[e], Lim<float>::lowest()), sx) : sx;
+    }
+  }
+  RowStat<float> r;
+  r.m = m;
+  r.s = warp_sum(s);
+  r.sx = ENT ? warp_sum(sx) : 0.f;
+  return r;
+}
+
 // K1 fixed shift: each thread takes its exp2 shift from its first chunk of the row
 // and keeps it (no per-chunk max / rescale afterwards); overflow (a later logit
 // > ~88 above the shift) shows up as a non-finite sum and the epilogue recomputes

@@ -252,9 +252,9 @@ template <> struct EFmt<float> { using V = Vec<float>; };
 
 // Pass-1 fold of one chunk held as raw words: warp-uniform running max, e computed
 // once, the e words returned in place of the logits and the shift c returned.
-template <typename T, bool ENT, bool FULL>
+template <typename T, bool ENT, bool FULL, bool UNAL>
 __device__ __forceinline__ float fold_to_e(RowStat<float>& rs, uint32_t (&w)[kTWords], int warp, int lane,
-                                           int nvec) {
+                                           int nvec, int e0, int V) {
   constexpr int E = Vec<T>::N;
   constexpr int N = kTV * E;
   float f[N];
@@ -262,9 +262,14 @@ __device__ __forceinline__ float fold_to_e(RowStat<float>& rs, uint32_t (&w)[kTW
   for (int j = 0; j < kTV; ++j) {
     float g[E];
     Vec<T>::unpack(make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]), g);
-    const bool ok = FULL || t_vec_index(warp, lane, j) < nvec;
+    // non-FULL: vectors past the chunk's data are padding; on unaligned rows element
+    // k of the chunk is row element e0 + k, valid in [0, V)
+    const int vi = t_vec_index(warp, lane, j);
+    const int i0 = e0 + vi * E;
 #pragma unroll
-    for (int e = 0; e < E; ++e) f[j * E + e] = ok ? g[e] : Lim<float>::ninf();
+    for (int e = 0; e < E; ++e)
+      f[j * E + e] = (FULL || (UNAL ? (i0 + e >= 0 && i0 + e < V) : vi < nvec)) ? g[e]
+                                                                             : Lim<float>::ninf();
   }
   // rs.m is warp-uniform; it stays -inf until a chunk with a finite value was seen
   const bool need_max = !kFixedShift || rs.m == Lim<float>::ninf();
@@ -312,27 +317,82 @@ __device__ __forceinline__ float fold_to_e(RowStat<float>& rs, uint32_t (&w)[kTW
 
 // Pass-1 step on one ring chunk: load this thread's words, fold them to e (returns
 // the shift c); full 32 KB chunks take the branch-free path.
-template <typename T, bool ENT>
+// Row geometry in the chunk stream: a row starting off a 16-byte boundary is loaded
+// from the boundary below it, so chunk element k is row element e0 + k with
+// e0 = c * per_chunk - head (head = the row's offset from that boundary, in elements).
+template <typename T>
+__device__ __forceinline__ bool region_valid(int warp, int e0, int V) {
+  constexpr int W = kTWBytes / 16, E = Vec<T>::N;
+  const int lo = e0 + warp * W * E;
+  return lo >= 0 && lo + (int64_t)W * E <= V;
+}
+template <typename T, bool ENT, bool UNAL>
 __device__ __forceinline__ float chunk_to_e(RowStat<float>& rs, const uint4* q, uint32_t (&wv)[kTWords],
-                                            int warp, int lane, int nvec) {
-  if ((warp + 1) * (kTWBytes / 16) <= nvec) {  // this warp's region all valid
+                                            int warp, int lane, int nvec, int e0, int V) {
+  if (UNAL ? region_valid<T>(warp, e0, V) : (warp + 1) * (kTWBytes / 16) <= nvec) {  // region all valid
     lds_raw<true>(q, warp, lane, nvec, wv);
-    return fold_to_e<T, ENT, true>(rs, wv, warp, lane, nvec);
+    return fold_to_e<T, ENT, true, UNAL>(rs, wv, warp, lane, nvec, e0, V);
   }
   lds_raw<false>(q, warp, lane, nvec, wv);
-  return fold_to_e<T, ENT, false>(rs, wv, warp, lane, nvec);
+  return fold_to_e<T, ENT, false, UNAL>(rs, wv, warp, lane, nvec, e0, V);
+}
+// Store one 16-byte vector of dlogits holding chunk elements [k, k + E) = row elements
+// [i0, i0 + E): whole when they are all in the row, else element by element.
+template <typename T>
+__device__ __forceinline__ void store_vec(uint4* dst, int vi, uint4 o, int i0, int V,
+                                          bool stream) {
+  constexpr int E = Vec<T>::N;
+  if (i0 >= 0 && i0 + E <= V) {
+    if (stream) __stcs(dst + vi, o);
+    else dst[vi] = o;
+    return;
+  }
+  const uint32_t w[4] = {o.x, o.y, o.z, o.w};
+  if constexpr (sizeof(T) == 2) {
+    unsigned short* d = reinterpret_cast<unsigned short*>(dst + vi);
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+      if (i0 + e >= 0 && i0 + e < V) d[e] = (unsigned short)(w[e >> 1] >> (16 * (e & 1)));
+  } else {
+    uint32_t* d = reinterpret_cast<uint32_t*>(dst + vi);
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+      if (i0 + e >= 0 && i0 + e < V) d[e] = w[e];
+  }
+}
+// Per-row stream geometry: the row's offset from the 16-byte boundary below it (the
+// chunk stream starts there) and the bytes of its last chunk.  Two ints, so they can
+// live across the whole row; the pointers are recomputed where needed.
+struct RowGeo {
+  int hb;            // head bytes: row element 0 sits at stream byte hb
+  int last_bytes;    // bytes of chunk nchunks - 1
+  template <typename T> __device__ __forceinline__ int head() const { return hb / (int)sizeof(T); }
+  __device__ __forceinline__ const char* src(const PpoArgs& a, int64_t row) const {
+    return a.logits + row * a.ld_in_bytes - hb;
+  }
+  __device__ __forceinline__ char* dst(const PpoArgs& a, int64_t row) const {
+    return a.dlogits + row * a.ld_out_bytes - hb;
+  }
+};
+template <typename T, bool UNAL>
+__device__ __forceinline__ RowGeo row_geo(const PpoArgs& a, int64_t row, int nchunks) {
+  RowGeo g;
+  g.hb = UNAL ? (int)((uintptr_t)(a.logits + row * a.ld_in_bytes) & 15) : 0;
+  const int64_t sb = (g.hb + a.vocab * (int64_t)sizeof(T) + 15) & ~(int64_t)15;
+  g.last_bytes = (int)(sb - (int64_t)(nchunks - 1) * kChunkBytes);
+  return g;
 }
 
 // Pass 2 of a streamed chunk: this thread's vectors of chunk c re-read from the
 // logits (last use: evict-first loads; in place safe, each thread reads exactly the
 // vectors it then overwrites), dlogits = g 2^(x log2e - lse).
-template <typename T>
-__device__ __forceinline__ void stream_chunk_dlogits(const PpoArgs& a, int64_t row, char* drow,
-                                                     int c, int nvec, int warp, int lane, float g,
-                                                     float lse_s) {
+template <typename T, bool UNAL>
+__device__ __forceinline__ void stream_chunk_dlogits(const PpoArgs& a, int64_t row, const RowGeo& geo,
+                                                     int V, char* drow, int c, int nvec,
+                                                     int warp, int lane, float g, float lse_s) {
   constexpr int E = Vec<T>::N;
-  const uint4* src = reinterpret_cast<const uint4*>(a.logits + row * a.ld_in_bytes) +
-                     (size_t)c * (kChunkBytes / 16);
+  const int e0 = c * (kChunkBytes / (int)sizeof(T)) - geo.head<T>();
+  const uint4* src = reinterpret_cast<const uint4*>(geo.src(a, row)) + (size_t)c * (kChunkBytes / 16);
   uint4* dst = reinterpret_cast<uint4*>(drow + (size_t)c * kChunkBytes);
   const float2 L2 = make_float2(Lim<float>::kLog2e, Lim<float>::kLog2e);
   const float2 C2 = make_float2(-lse_s, -lse_s);
@@ -356,12 +416,15 @@ __device__ __forceinline__ void stream_chunk_dlogits(const PpoArgs& a, int64_t r
         f[e] = d.x;
         f[e + 1] = d.y;
       }
-      st_out(&dst[vi], Vec<T>::pack(f), (kL2Hints & 2) != 0);
+      if constexpr (UNAL) store_vec<T>(dst, vi, Vec<T>::pack(f), e0 + vi * E, V, (kL2Hints & 2) != 0);
+      else st_out(&dst[vi], Vec<T>::pack(f), (kL2Hints & 2) != 0);
     }
   }
 }
 
-template <typename T, bool ENT>
+// UNAL: rows that may start off a 16-byte boundary (separate instantiation, so the
+// aligned rows' kernel keeps its register allocation).
+template <typename T, bool ENT, bool UNAL>
 __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
   static_assert(sizeof(T) == 2 || sizeof(T) == 4, "TMEM K2 path: 16/32-bit logits");
   using A = float;
@@ -375,9 +438,12 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
   __shared__ uint32_t s_tmem_base;
 
   const int64_t row_bytes = a.vocab * (int64_t)sizeof(T);
-  const int nfull = (int)(row_bytes / kChunkBytes);
-  const int last_bytes = (int)(row_bytes - (int64_t)nfull * kChunkBytes);
-  const int nchunks = nfull + (last_bytes > 0 ? 1 : 0);
+  // chunks per row: the same for every row (the host checks that an unaligned row's
+  // extra head bytes never add a chunk)
+  const int nchunks = (int)((((row_bytes + 15) & ~(int64_t)15) + kChunkBytes - 1) / kChunkBytes);
+  const int per_chunk = kChunkBytes / (int)sizeof(T);
+  const int V = (int)a.vocab;  // < 2^31 (checked on the host)
+  auto nvec_of = [&](int c, const RowGeo& g) { return (c < nchunks - 1 ? kChunkBytes : g.last_bytes) / 16; };
   const int ntm = min(nchunks, kTmemChunks);     // chunks parked in TMEM
   const int R = min(nchunks - ntm, kTResMax);  // resident tail chunks
   const int S = nchunks - ntm - R;               // streamed chunks [ntm, ntm + S)
@@ -417,11 +483,12 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
       uint32_t used = 0;
       const uint64_t pol_keep = l2_policy_evict_last(), pol_drop = l2_policy_evict_first();
       for (int64_t row = cid; row < a.n_rows; row += ncl) {
-        const char* src = a.logits + row * a.ld_in_bytes;
+        const RowGeo geo = row_geo<T, UNAL>(a, row, nchunks);
+        const char* src = geo.src(a, row);
         for (int c = 0; c < nchunks; ++c) {
           if (used >= nslots) mbar_wait(&empty[cur.slot], cur.phase ^ 1u);
           else ++used;
-          const uint32_t bytes = (uint32_t)(c < nfull ? kChunkBytes : last_bytes);
+          const uint32_t bytes = (uint32_t)(c < nchunks - 1 ? kChunkBytes : geo.last_bytes);
           mbar_arrive_expect_tx(&full[cur.slot], bytes);
           if ((kL2Hints & 1) && S > 0)
             bulk_g2s_hint(ring + (size_t)cur.slot * kChunkBytes, src + (size_t)c * kChunkBytes,
@@ -461,7 +528,11 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
       }
       RowStat<A> tot = warp_merge(w);
       const bool slow = kFixedShift && !(tot.s < INFINITY);  // overflow (or NaN logits)
-      if (slow) tot = row_stats_global<T, ENT>(a, row, 0, (a.vocab * (int64_t)sizeof(T)) / 16, lane);
+      if (slow) {
+        const int hb = (int)((uintptr_t)(a.logits + row * a.ld_in_bytes) & 15);
+        if constexpr (UNAL) tot = row_stats_masked<T, ENT>(a, row, hb, lane);
+        else tot = row_stats_global<T, ENT>(a, row, 0, (a.vocab * (int64_t)sizeof(T)) / 16, lane);
+      }
       const A lse_s = Ex<A>::lse_shift(tot.m == Lim<A>::ninf() ? A(0) : tot.m, tot.s);
       const double lse = Ex<A>::lse_nat(lse_s);
       const double ent = ENT ? lse - (double)(tot.sx / tot.s) : 0.0;
@@ -502,10 +573,11 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
     for (int64_t row = cid; row < a.n_rows; row += ncl, ++it) {
       const int par = it & 1;
       float* cw = &tail->cw[par][0][0];  // [chunk][warp]
+      const RowGeo geo = row_geo<T, UNAL>(a, row, nchunks);
       // ---- park the lookahead chunks (their e is in the ring slots) in TMEM
       Cursor cc = cur;
       for (int c = 0; c < la; ++c) {
-        const int nvec = (c < nfull ? kChunkBytes : last_bytes) / 16;
+        const int nvec = nvec_of(c, geo);
         uint32_t wv[kTWords];
         lds_raw(reinterpret_cast<const uint4*>(ring + (size_t)cc.slot * kChunkBytes), warp, lane,
                 nvec, wv);
@@ -518,10 +590,11 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
       RowStat<A> rs = carry;
       for (int c = la; c < nchunks; ++c) {
         mbar_wait(&full[cc.slot], cc.phase);
-        const int nvec = (c < nfull ? kChunkBytes : last_bytes) / 16;
+        const int nvec = nvec_of(c, geo);
         uint4* q = reinterpret_cast<uint4*>(ring + (size_t)cc.slot * kChunkBytes);
         uint32_t wv[kTWords];
-        const float cshift = chunk_to_e<T, ENT>(rs, q, wv, warp, lane, nvec);
+        const float cshift =
+            chunk_to_e<T, ENT, UNAL>(rs, q, wv, warp, lane, nvec, c * per_chunk - geo.head<T>(), V);
         if (c < ntm) {
           if (lane == 0) cw[c * kTW + warp] = cshift;
           tmem_stw(tmem_addr(tbase, warp, c), wv);
@@ -552,12 +625,14 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
       RowStat<A> nxt;
       nxt.init();
       Cursor lc = after;
+      const RowGeo geo_n = (UNAL && has_next) ? row_geo<T, UNAL>(a, row + ncl, nchunks) : geo;
       for (int c = 0; c < la_next; ++c) {
         mbar_wait(&full[lc.slot], lc.phase);
-        const int nvec = (c < nfull ? kChunkBytes : last_bytes) / 16;
+        const int nvec = nvec_of(c, geo_n);
         uint4* q = reinterpret_cast<uint4*>(ring + (size_t)lc.slot * kChunkBytes);
         uint32_t wv[kTWords];
-        const float cshift = chunk_to_e<T, ENT>(nxt, q, wv, warp, lane, nvec);
+        const float cshift =
+            chunk_to_e<T, ENT, UNAL>(nxt, q, wv, warp, lane, nvec, c * per_chunk - geo_n.head<T>(), V);
         if (lane == 0) cwn[c * kTW + warp] = cshift;
         sts_raw(q, warp, lane, nvec, wv);
         lc.next(nslots);
@@ -570,7 +645,7 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
       const float g = (float)b.gc;
       const float lse_s = (float)b.lse;
       const T dtok = from_bits<T>(b.dtok);
-      char* drow = a.dlogits + row * a.ld_out_bytes;
+      char* drow = geo.dst(a, row);  // chunk-stream base of this row's dlogits
       // ---- pass 2: dlogits = e * g 2^(c - lse), 16-byte stores.  Full chunks are
       // branch-free; the one-hot element is patched afterwards by the thread that
       // stored its vector (same-thread program order => the patch lands last).
@@ -579,13 +654,14 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
       if (kFixedShift && b.slow) {
         // slow path: dlogits = g 2^(x log2e - lse) rebuilt from the row in HBM (each
         // thread reads exactly the vectors it then overwrites: in-place safe)
-        const uint4* xrow = reinterpret_cast<const uint4*>(a.logits + row * a.ld_in_bytes);
+        const uint4* xrow = reinterpret_cast<const uint4*>(geo.src(a, row));
         const float2 L2 = make_float2(Lim<float>::kLog2e, Lim<float>::kLog2e);
         const float2 C2 = make_float2(-lse_s, -lse_s);
         const float2 G2 = make_float2(g, g);
         Cursor cs = cur;
         for (int c = 0; c < nchunks; ++c) {
-          const int nvec = (c < nfull ? kChunkBytes : last_bytes) / 16;
+          const int nvec = nvec_of(c, geo);
+          const int e0 = c * per_chunk - geo.head<T>();
           if (c >= ntm + S) {  // resident tail chunk: release its ring slot as usual
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[cs.slot]);
@@ -605,7 +681,8 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
                 f[e] = d.x;
                 f[e + 1] = d.y;
               }
-              dst[vi] = Vec<T>::pack(f);
+              if constexpr (UNAL) store_vec<T>(dst, vi, Vec<T>::pack(f), e0 + vi * E, V, false);
+              else dst[vi] = Vec<T>::pack(f);
             }
           }
           cs.next(nslots);
@@ -619,11 +696,13 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
                       : k < R ? nchunks - R + k
                       : kP2Order == 1 ? (k < R + S ? ntm + (k - R) : k - R - S)
                                       : k - R;
-        const int nvec = (c < nfull ? kChunkBytes : last_bytes) / 16;
-        const bool full = (warp + 1) * (kTWBytes / 16) <= nvec;  // this warp's region
+        const int nvec = nvec_of(c, geo);
+        const int e0 = c * per_chunk - geo.head<T>();
+        const bool full = UNAL ? region_valid<T>(warp, e0, V)
+                               : (warp + 1) * (kTWBytes / 16) <= nvec;  // this warp's region
         uint32_t wv[kTWords];
         if (c >= ntm && c < ntm + S) {  // streamed chunk: dlogits from the logits
-          stream_chunk_dlogits<T>(a, row, drow, c, nvec, warp, lane, g, lse_s);
+          stream_chunk_dlogits<T, UNAL>(a, row, geo, V, drow, c, nvec, warp, lane, g, lse_s);
           continue;
         }
         if (c < ntm) {
@@ -645,6 +724,11 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
         // relative, inside the bf16 contract) instead of unpack + FMUL2 + repack.
         constexpr bool kPackedMul = std::is_same<T, __nv_bfloat16>::value && kK2PackedBf16Mul;
         const __nv_bfloat162 Fb = __float2bfloat162_rn(F);
+        auto put = [&](int j, uint4 o) {
+          const int vi = t_vec_index(warp, lane, j);
+          if (!UNAL || full) st_out(&dst[vi], o, st_stream);
+          else store_vec<T>(dst, vi, o, e0 + vi * E, V, st_stream);
+        };
         auto scale_store = [&](int j) {
           if constexpr (kPackedMul) {
             uint4 o;
@@ -652,7 +736,7 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
             o.y = bf162_bits(__hmul2(bits_bf162(wv[4 * j + 1]), Fb));
             o.z = bf162_bits(__hmul2(bits_bf162(wv[4 * j + 2]), Fb));
             o.w = bf162_bits(__hmul2(bits_bf162(wv[4 * j + 3]), Fb));
-            st_out(&dst[t_vec_index(warp, lane, j)], o, st_stream);
+            put(j, o);
           } else {
             float f[E];
             EFmt<T>::V::unpack(make_uint4(wv[4 * j], wv[4 * j + 1], wv[4 * j + 2], wv[4 * j + 3]), f);
@@ -662,7 +746,7 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
               f[e] = d.x;
               f[e + 1] = d.y;
             }
-            st_out(&dst[t_vec_index(warp, lane, j)], Vec<T>::pack(f), st_stream);
+            put(j, Vec<T>::pack(f));
           }
         };
         if (full) {  // branch-free
@@ -675,13 +759,13 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
         }
       }
       }  // fast path
-      {  // the one-hot element: owner of vector vt of chunk ct
-        const int64_t per_chunk = kChunkBytes / (int)sizeof(T);
+      {  // the one-hot element: owner of vector vt of chunk ct (stream index st)
         if (b.tok >= 0 && b.tok < a.vocab) {
-          const int ct = (int)(b.tok / per_chunk);
-          const int vt = (int)((b.tok - (int64_t)ct * per_chunk) / E);
+          const int64_t st = b.tok + geo.head<T>();
+          const int ct = (int)(st / per_chunk);
+          const int vt = (int)((st - (int64_t)ct * per_chunk) / E);
           if (warp == vt / (kTWBytes / 16) && lane == (vt & 31))
-            reinterpret_cast<T*>(drow)[b.tok] = dtok;
+            reinterpret_cast<T*>(drow)[st] = dtok;
         }
       }
       cur = after;

@@ -616,3 +616,36 @@ def test_unaligned_rows_cta_kernel(dt, V):
     g = logits.cuda()
     dl2, st2 = K.ppo_fwd_bwd(g, cuda(tokens), cuda(behav), cuda(prox), cuda(adv), dlogits=g)
     check_k2(dt, dl2.double().cpu().numpy(), st2.cpu().numpy(), ref, T)
+
+
+@pytest.mark.parametrize("dt,V", [("bf16", 50257), ("f32", 50257), ("bf16", 151937),
+                                  ("f16", 100003), ("bf16", 262145), ("f32", 151937),
+                                  ("bf16", 16381)])
+def test_unaligned_rows_tmem_kernel(dt, V):
+    """Unaligned rows with dlogits at the logits' 16-byte phase run the TMEM K2 from the
+    boundary below each row (masked head / tail elements, per-row last chunk), incl.
+    streamed chunks (bf16 262,145 / fp32 151,937) and a shape whose head bytes could
+    add a chunk (bf16 16,381: falls back to the row-CTA kernel).  Entropy, lp, in place,
+    the one-hot element at both row ends and an overflow row vs the float64 oracle."""
+    T = 37
+    logits, x64, tokens, behav, prox, adv = make_case(T, V, dt, seed=V % 53)
+    tokens[0], tokens[1], tokens[2] = 0, V - 1, V // 2
+    lg = logits.clone()
+    lg[3, : V // 3] = -50.0                   # overflow above the fixed shift
+    lg[3, V - 7:] = 70.0 if dt != "f16" else 60.0
+    x64 = lg.double().numpy()
+    lp_ref = O.token_logprobs(x64, tokens)
+    prox = lp_ref + 0.03
+    behav = prox + 0.1
+    ref = O.surrogate_terms(x64, tokens, behav, prox, adv)
+    for in_place in (False, True):
+        g = lg.cuda()
+        lp = torch.zeros(T, dtype=torch.float64, device="cuda")
+        ent = torch.zeros(T, dtype=torch.float64, device="cuda")
+        dl, st = K.ppo_fwd_bwd(g, cuda(tokens), cuda(behav), cuda(prox), cuda(adv),
+                               dlogits=g if in_place else None, lp_out=lp, entropy_out=ent)
+        check_k2(dt, dl.double().cpu().numpy(), st.cpu().numpy(), ref, T)
+        ok, err = rel_close(lp.cpu().numpy(), lp_ref, TOL[dt])
+        assert ok, err
+        assert np.allclose(ent.cpu().numpy(), O.token_entropy(x64), rtol=TOL[dt],
+                           atol=TOL[dt] * 10)
