@@ -63,8 +63,10 @@ typedef enum { AREAL_F32 = 0, AREAL_BF16 = 1, AREAL_F16 = 2, AREAL_F64 = 3 } are
  * K2 on 16-bit rows and on fp32 rows larger than one CTA's shared memory -> the
  * Tensor-Memory kernel (8 x 32 KB parked in TMEM, up to 7 resident in the ring, the
  * rest streamed); other K2 rows (fp32 / fp64 that fit, fp64 beyond via a cluster
- * split) and all of K1 -> ROW_RING (TMA bulk ring).  Unaligned rows of >= 16 KB ->
- * one CTA per row; rows under 16 KB -> ROW_WARP (one warp per row).  ROW_RING /
+ * split) and all of K1 -> ROW_RING (TMA bulk ring).  Unaligned rows of >= 16 KB:
+ * K2 on 16/32-bit rows -> the TMEM kernel (masked 16-byte-aligned loads) when dlogits
+ * share the logits' 16-byte phase, otherwise (and all of K1) one CTA per row; rows
+ * under 16 KB -> ROW_WARP (one warp per row).  ROW_RING /
  * ROW_WARP force the respective family. */
 typedef enum { AREAL_ALGO_AUTO = 0, AREAL_ALGO_ROW_WARP = 1, AREAL_ALGO_ROW_RING = 2 } areal_algo_t;
 

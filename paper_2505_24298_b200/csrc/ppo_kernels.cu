@@ -9,7 +9,8 @@
 //   row_warp : one warp per row, any vocab / alignment; both passes read global
 //              memory (the second pass hits L1/L2).  Rows under 16 KB.
 //   row_cta  : one CTA per row for rows >= 16 KB that are not 16-byte aligned
-//              (scalar head / 16-byte-vector body / scalar tail; K2 re-reads from L2).
+//              (scalar head / 16-byte-vector body / scalar tail; K2 re-reads from L2):
+//              all such K1 rows, and K2 rows the TMEM kernel cannot take.
 //   row_ring : persistent, warp-specialised (ppo_ring.cuh).  A producer thread
 //              streams each row through a ring of 32 KB shared-memory chunks with
 //              1-D TMA bulk copies (cp.async.bulk + mbarrier complete_tx).  K1 frees
@@ -21,7 +22,8 @@
 //              (ppo_tmem.cuh): the row's first 8 chunks are parked in Tensor Memory as
 //              e = 2^(x - c), up to 7 more stay resident in the ring, any further
 //              middle chunks are streamed and re-read from L2 in pass 2; one CTA per
-//              row (the bf16 V ~ 152K default).
+//              row (the bf16 V ~ 152K default).  Unaligned 16/32-bit rows too (UNAL
+//              instantiation: bulk copies from the 16-byte boundary below the row).
 // HBM traffic = one logits read (+ one dlogits write for K2) per element.
 #include <cstdlib>
 #include <type_traits>
