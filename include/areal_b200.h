@@ -65,8 +65,9 @@ typedef enum { AREAL_F32 = 0, AREAL_BF16 = 1, AREAL_F16 = 2, AREAL_F64 = 3 } are
  * rest streamed); other K2 rows (fp32 / fp64 that fit, fp64 beyond via a cluster
  * split) and all of K1 -> ROW_RING (TMA bulk ring).  Unaligned rows of >= 16 KB:
  * K2 on 16/32-bit rows -> the TMEM kernel (masked 16-byte-aligned loads) when dlogits
- * share the logits' 16-byte phase, otherwise (and all of K1) one CTA per row; rows
- * under 16 KB -> ROW_WARP (one warp per row).  ROW_RING /
+ * share the logits' 16-byte phase; K1 on long rows -> the ring kernel (masked
+ * 16-byte-aligned loads); otherwise one CTA per row; rows under 16 KB -> ROW_WARP
+ * (one warp per row).  ROW_RING /
  * ROW_WARP force the respective family. */
 typedef enum { AREAL_ALGO_AUTO = 0, AREAL_ALGO_ROW_WARP = 1, AREAL_ALGO_ROW_RING = 2 } areal_algo_t;
 

@@ -10,7 +10,8 @@
 //              memory (the second pass hits L1/L2).  Rows under 16 KB.
 //   row_cta  : one CTA per row for rows >= 16 KB that are not 16-byte aligned
 //              (scalar head / 16-byte-vector body / scalar tail; K2 re-reads from L2):
-//              all such K1 rows, and K2 rows the TMEM kernel cannot take.
+//              shorter K1 rows and K2 rows the TMEM kernel cannot take (long unaligned
+//              K1 rows run the ring kernel's UNAL instantiation).
 //   row_ring : persistent, warp-specialised (ppo_ring.cuh).  A producer thread
 //              streams each row through a ring of 32 KB shared-memory chunks with
 //              1-D TMA bulk copies (cp.async.bulk + mbarrier complete_tx).  K1 frees
@@ -580,9 +581,9 @@ template <typename T>
 __global__ void __launch_bounds__(kWarpKernelWarps * 32) ppo_warp_kernel(PpoArgs a) {
   row_warp_body<T, true>(a);
 }
-template <typename T, bool ENT>
+template <typename T, bool ENT, bool UNAL = false>
 __global__ void __launch_bounds__(kRingThreads, 1) logprob_ring_kernel(PpoArgs a) {
-  row_ring_body<T, false, ENT>(a);
+  row_ring_body<T, false, ENT, UNAL>(a);
 }
 template <typename T, bool ENT>
 __global__ void __launch_bounds__(kRingThreads, 1) ppo_ring_kernel(PpoArgs a) {
@@ -733,6 +734,38 @@ static int launch_ring(PpoArgs a, cudaStream_t stream, int cs_force) {
   return AREAL_OK;
 }
 
+// K1 on rows off a 16-byte boundary: the ring kernel's UNAL instantiation (bulk
+// copies from the boundary below each row, masked edge elements), one CTA per SM.
+template <typename T, bool ENT>
+static int launch_ring_k1_unal(PpoArgs a, cudaStream_t stream) {
+  DevInfo d = get_dev();
+  const int nslots = max_slots(d);
+  a.cluster_size = 1;
+  a.slice16 = (a.vocab * (int64_t)sizeof(T)) / 16;
+  a.nslots = nslots;
+  const size_t smem = ring_smem_bytes(nslots);
+  auto kern = logprob_ring_kernel<T, ENT, true>;
+  static thread_local int attr_set[16] = {0};
+  const int dev = d.dev & 15;
+  if (!attr_set[dev]) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return AREAL_ERR_CUDA;
+    attr_set[dev] = 1;
+  }
+  const int64_t grid = std::min<int64_t>(a.n_rows, (int64_t)d.sms);
+  kern<<<(unsigned)grid, kRingThreads, smem, stream>>>(a);
+  AREAL_CUDA_CHECK_LAUNCH();
+  return AREAL_OK;
+}
+
+// Unaligned rows of 16/32-bit logits whose head bytes never add a 32 KB chunk.
+static bool unaligned_chunks_ok(const PpoArgs& a, int es) {
+  const int64_t rb = a.vocab * es;
+  if (rb < 16384 || a.vocab >= ((int64_t)1 << 30) || !(es == 2 || es == 4)) return false;
+  const int64_t lo = (rb + 15) & ~(int64_t)15, hi = (rb + 16 - es + 15) & ~(int64_t)15;
+  return (lo + kChunkBytes - 1) / kChunkBytes == (hi + kChunkBytes - 1) / kChunkBytes;
+}
+
 template <typename T, bool BWD>
 static int launch_warp(PpoArgs a, cudaStream_t stream) {
   DevInfo d = get_dev();
@@ -784,6 +817,14 @@ static bool tmem_unaligned_ok(const PpoArgs& a, int es) {
   return (lo + kChunkBytes - 1) / kChunkBytes == (hi + kChunkBytes - 1) / kChunkBytes;
 }
 
+static bool k1_unal_off() {  // AREAL_K1_RING_UNALIGNED=0: unaligned K1 rows on the row-CTA kernel
+  static const bool off = [] {
+    const char* s = getenv("AREAL_K1_RING_UNALIGNED");
+    return s && atoi(s) == 0;
+  }();
+  return off;
+}
+
 static bool rowcta_off() {  // AREAL_ROWCTA=0: unaligned rows on the one-warp kernel
   static const bool off = [] {
     const char* s = getenv("AREAL_ROWCTA");
@@ -832,6 +873,20 @@ static int dispatch(PpoArgs a, int dtype, int algo, cudaStream_t stream) {
         default: break;
       }
       if (rc != AREAL_ERR_UNSUPPORTED) return rc;
+    }
+  }
+  // unaligned K1 rows: the ring kernel from the 16-byte boundary below each row
+  // (long rows only: below ~160 KB (16-bit) / 256 KB (fp32) the row-CTA kernel's 8 rows
+  // per SM hide the per-row epilogue better; profiles/r01_rowcta_sweep.txt)
+  const bool k1_ring_long = a.vocab * es >= (es == 2 ? 160 * 1024 : 256 * 1024);
+  if (!BWD && !aligned && algo == AREAL_ALGO_AUTO && k1_ring_long && unaligned_chunks_ok(a, es) &&
+      !k1_unal_off()) {
+    const bool ent = a.ent_out != nullptr;
+    switch (dtype) {
+      case AREAL_F32: return ent ? launch_ring_k1_unal<float, true>(a, stream) : launch_ring_k1_unal<float, false>(a, stream);
+      case AREAL_BF16: return ent ? launch_ring_k1_unal<__nv_bfloat16, true>(a, stream) : launch_ring_k1_unal<__nv_bfloat16, false>(a, stream);
+      case AREAL_F16: return ent ? launch_ring_k1_unal<__half, true>(a, stream) : launch_ring_k1_unal<__half, false>(a, stream);
+      default: break;
     }
   }
   // unaligned (or ring-refused) rows of >= 16 KB: one CTA per row, body in 16-byte vectors

@@ -81,12 +81,17 @@ __device__ __forceinline__ int vec_index(int warp, int lane, int j) {
 }
 
 // Load this thread's vectors of a chunk (nvec valid vectors) as accumulation values.
-template <typename T>
+// UNAL (K1 on rows off a 16-byte boundary): chunk element k is row element e0 + k and
+// only [0, V) of the row counts.
+template <typename T, bool UNAL = false>
 __device__ __forceinline__ void load_values(const uint4* q, int warp, int lane, int nvec,
-                                            typename Traits<T>::Acc* f) {
+                                            typename Traits<T>::Acc* f, int e0 = 0, int V = 0) {
   using A = typename Traits<T>::Acc;
   constexpr int E = Vec<T>::N;
-  if ((warp + 1) * (kWarpBytes / 16) <= nvec) {  // this warp's 2 KB all valid: branch-free
+  const bool whole = UNAL ? (e0 + warp * (kWarpBytes / 16) * E >= 0 &&
+                             e0 + (warp + 1) * (kWarpBytes / 16) * E <= V)
+                          : (warp + 1) * (kWarpBytes / 16) <= nvec;
+  if (whole) {  // this warp's 2 KB all valid: branch-free
 #pragma unroll
     for (int j = 0; j < kVecPerThread; ++j) {
       A g[E];
@@ -106,7 +111,10 @@ __device__ __forceinline__ void load_values(const uint4* q, int warp, int lane, 
         for (int e = 0; e < E; ++e) g[e] = Lim<A>::ninf();
       }
 #pragma unroll
-      for (int e = 0; e < E; ++e) f[j * E + e] = g[e];
+      for (int e = 0; e < E; ++e) {
+        const int i = e0 + vi * E + e;
+        f[j * E + e] = (!UNAL || (i >= 0 && i < V)) ? g[e] : Lim<A>::ninf();
+      }
     }
   }
 }
@@ -315,8 +323,9 @@ template <typename T> __device__ __forceinline__ T from_bits(unsigned long long 
   return v;
 }
 
-template <typename T, bool BWD, bool ENT>
+template <typename T, bool BWD, bool ENT, bool UNAL = false>
 __device__ __forceinline__ void row_ring_body(const PpoArgs& a) {
+  static_assert(!UNAL || !BWD, "unaligned rows: K1 only (K2 runs the TMEM kernel)");
   using A = typename Traits<T>::Acc;
   constexpr int E = Vec<T>::N;                 // elements per 16 bytes
   constexpr int NV = kVecPerThread * E;        // values per thread per chunk
@@ -340,7 +349,18 @@ __device__ __forceinline__ void row_ring_body(const PpoArgs& a) {
   const int slice_bytes = e16 > b16 ? (int)((e16 - b16) * 16) : 0;  // < 2^31 (checked on host)
   const int nfull = slice_bytes / kChunkBytes;
   const int last_bytes = slice_bytes - nfull * kChunkBytes;
-  const int nchunks = nfull + (last_bytes > 0 ? 1 : 0);
+  // UNAL: V16 rounds the row down, so count chunks on the 16-byte-rounded-up row
+  const int nchunks = UNAL ? (int)((((a.vocab * (int64_t)sizeof(T) + 15) & ~(int64_t)15) + kChunkBytes - 1) / kChunkBytes)
+                           : nfull + (last_bytes > 0 ? 1 : 0);
+  // per row (UNAL): head bytes below the row start, bytes of the last chunk
+  auto row_hb = [&](int64_t row) {
+    return UNAL ? (int)((uintptr_t)(a.logits + row * a.ld_in_bytes) & 15) : 0;
+  };
+  auto chunk_bytes = [&](int c, int hb) {
+    if (!UNAL) return c < nfull ? kChunkBytes : last_bytes;
+    const int64_t sb = (hb + a.vocab * (int64_t)sizeof(T) + 15) & ~(int64_t)15;
+    return c < nchunks - 1 ? kChunkBytes : (int)(sb - (int64_t)(nchunks - 1) * kChunkBytes);
+  };
   const int64_t slice_e0 = b16 * E;  // first vocab element of this rank's slice
 
   const int tid = threadIdx.x;
@@ -367,11 +387,12 @@ __device__ __forceinline__ void row_ring_body(const PpoArgs& a) {
       Cursor cur = {0u, 0u};
       uint32_t used = 0;  // slots filled at least once (no wait needed on first use)
       for (int64_t row = cid; row < a.n_rows; row += ncl) {
-        const char* src = a.logits + row * a.ld_in_bytes + b16 * 16;
+        const int hb = row_hb(row);
+        const char* src = a.logits + row * a.ld_in_bytes + b16 * 16 - hb;
         for (int c = 0; c < nchunks; ++c) {
           if (used >= nslots) mbar_wait(&empty[cur.slot], cur.phase ^ 1u);
           else ++used;
-          const uint32_t bytes = (uint32_t)(c < nfull ? kChunkBytes : last_bytes);
+          const uint32_t bytes = (uint32_t)chunk_bytes(c, hb);
           mbar_arrive_expect_tx(&full[cur.slot], bytes);
           bulk_g2s(ring + (size_t)cur.slot * kChunkBytes, src + (size_t)c * kChunkBytes, bytes,
                    &full[cur.slot]);
@@ -413,8 +434,10 @@ __device__ __forceinline__ void row_ring_body(const PpoArgs& a) {
       w = warp_merge(w);  // every lane holds the CTA total
       if (!BWD && lane == 0) mbar_arrive(&tail->bcbar[par]);  // K1: partials consumed
       if constexpr (kFold1Fixed) {
-        if (!(w.s < INFINITY))  // fixed-shift overflow (or NaN): exact, from HBM
-          w = row_stats_global<T, ENT>(a, row, b16, e16, lane);
+        if (!(w.s < INFINITY)) {  // fixed-shift overflow (or NaN): exact, from HBM
+          if constexpr (UNAL) w = row_stats_masked<T, ENT>(a, row, row_hb(row), lane);
+          else w = row_stats_global<T, ENT>(a, row, b16, e16, lane);
+        }
       }
       RowStat<A> tot = w;
       if (CS > 1) {
@@ -488,12 +511,14 @@ __device__ __forceinline__ void row_ring_body(const PpoArgs& a) {
       // ---- pass 1: online (max, sum e, sum e*x) over the chunks as they land
       RowStat<A> rs = carry;
       Cursor cc = pstart;
+      const int hb = row_hb(row);
       for (int c = la; c < nchunks; ++c) {
         mbar_wait(&full[cc.slot], cc.phase);
-        const int nvec = (c < nfull ? kChunkBytes : last_bytes) / 16;
+        const int nvec = chunk_bytes(c, hb) / 16;
         const uint4* q = reinterpret_cast<const uint4*>(ring + (size_t)cc.slot * kChunkBytes);
         A f[NV];
-        load_values<T>(q, warp, lane, nvec, f);
+        load_values<T, UNAL>(q, warp, lane, nvec, f, c * (kChunkBytes / (int)sizeof(T)) - hb / (int)sizeof(T),
+                             (int)a.vocab);
         if (!BWD) {  // K1: the slot is free as soon as the values are in registers
           if (kK1ArriveAllLanes) {
             mbar_arrive(&empty[cc.slot]);

@@ -638,6 +638,11 @@ def test_unaligned_rows_tmem_kernel(dt, V):
     prox = lp_ref + 0.03
     behav = prox + 0.1
     ref = O.surrogate_terms(x64, tokens, behav, prox, adv)
+    # K1 on the same rows (the ring kernel's unaligned instantiation; row-CTA at 16,381)
+    lp1, ent1 = K.logprob_fwd(lg.cuda(), cuda(tokens))
+    ok, err = rel_close(lp1.cpu().numpy(), lp_ref, TOL[dt])
+    assert ok, err
+    assert np.allclose(ent1.cpu().numpy(), O.token_entropy(x64), rtol=TOL[dt], atol=TOL[dt] * 10)
     for in_place in (False, True):
         g = lg.cuda()
         lp = torch.zeros(T, dtype=torch.float64, device="cuda")
