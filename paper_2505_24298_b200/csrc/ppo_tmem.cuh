@@ -339,6 +339,8 @@ __device__ __forceinline__ float chunk_to_e(RowStat<float>& rs, const uint4* q, 
 // Store one 16-byte vector of dlogits holding chunk elements [k, k + E) = row elements
 // [i0, i0 + E): whole when they are all in the row, else element by element.
 template <typename T>
+__device__ __noinline__ void store_vec_part(uint4* dst, int vi, uint4 o, int i0, int V);
+template <typename T>
 __device__ __forceinline__ void store_vec(uint4* dst, int vi, uint4 o, int i0, int V,
                                           bool stream) {
   constexpr int E = Vec<T>::N;
@@ -347,6 +349,12 @@ __device__ __forceinline__ void store_vec(uint4* dst, int vi, uint4 o, int i0, i
     else dst[vi] = o;
     return;
   }
+  store_vec_part<T>(dst, vi, o, i0, V);  // a row's first / last vector (rare: out of line)
+}
+// The in-row elements of one vector, element by element.
+template <typename T>
+__device__ __noinline__ void store_vec_part(uint4* dst, int vi, uint4 o, int i0, int V) {
+  constexpr int E = Vec<T>::N;
   const uint32_t w[4] = {o.x, o.y, o.z, o.w};
   if constexpr (sizeof(T) == 2) {
     unsigned short* d = reinterpret_cast<unsigned short*>(dst + vi);
