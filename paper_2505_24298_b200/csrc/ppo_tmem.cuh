@@ -28,8 +28,13 @@
 // kTResMax chunks resident (all 7 ring slots by default: 8 in TMEM, 7 resident, 4
 // streamed for that row); the S chunks between the TMEM part and the resident tail
 // are "streamed": folded in pass 1, slot freed at once, and re-read from global
-// memory in pass 2 (recently loaded, mostly from L2), dlogits = g 2^(x log2e - lse).
+// memory in pass 2 (kept in L2 by evict_last load hints), dlogits = g 2^(x log2e - lse).
 // Streamed chunks free their slot in pass 1, so the liveness bound above holds.
+//
+// Rows that start off a 16-byte boundary (UNAL instantiation) are loaded from the
+// boundary below them: chunk element k is row element c * per_chunk + k - head, the
+// elements outside the row are masked to -inf in pass 1 and not written in pass 2
+// (a row's first and last vectors are stored element by element).
 #pragma once
 
 namespace areal {
