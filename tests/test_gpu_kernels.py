@@ -654,3 +654,29 @@ def test_unaligned_rows_tmem_kernel(dt, V):
         assert ok, err
         assert np.allclose(ent.cpu().numpy(), O.token_entropy(x64), rtol=TOL[dt],
                            atol=TOL[dt] * 10)
+
+
+def test_unaligned_tmem_gather_prox_from_lp_versions():
+    """TMEM K2 on unaligned rows combined with the hot path's other inputs: a packed
+    row_index gather, prox_from_lp (first minibatch), per-token versions with an
+    eta staleness mask and a behaviour-weight cap, grad_scale; vs the oracle."""
+    T, V, dt = 29, 151937, "bf16"
+    logits, x64, tokens, behav, _, adv = make_case(T, V, dt, seed=808)
+    rng = np.random.default_rng(808)
+    versions = rng.integers(90, 101, size=T).astype(np.int32)
+    order = rng.permutation(T)
+    lg = logits[torch.from_numpy(order)].cuda()              # packed rows
+    ref = O.surrogate_terms(x64, tokens, behav, None, adv, versions=versions,
+                            current_version=100, eta_mask=4, behav_weight_cap=5.0,
+                            grad_scale=-0.25)
+    lp = torch.zeros(T, dtype=torch.float64, device="cuda")
+    dl, st = K.ppo_fwd_bwd(lg, cuda(tokens), cuda(behav), None, cuda(adv),
+                           versions=cuda(versions), current_version=100, eta_mask=4,
+                           behav_weight_cap=5.0, grad_scale=-0.25,
+                           row_index=cuda(order.astype(np.int32)), prox_from_lp=True,
+                           lp_out=lp)
+    got = np.empty((T, V))
+    got[order] = dl.double().cpu().numpy()
+    check_k2(dt, got, st.cpu().numpy(), ref, T)
+    ok, err = rel_close(lp.cpu().numpy(), ref["lp"], TOL[dt])
+    assert ok, err
