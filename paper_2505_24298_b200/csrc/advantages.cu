@@ -16,7 +16,7 @@
 
 namespace areal {
 
-constexpr int kMaxTreeDepth = 14;  // <= 16384 subtree roots
+constexpr int kMaxTreeDepth = 15;  // <= 32768 subtree roots (256 KB of the K3 workspace half)
 
 struct AdvArgs {
   const double* rewards;
@@ -133,11 +133,11 @@ __global__ void pw_top_kernel(const double* sums, int64_t n, int depth, int pass
     const int per = nodes / 4096;  // power of two
     for (int i = tid; i < 4096; i += blockDim.x) {
       // combine `per` consecutive leaves as a perfect binary tree
-      double v[4];
-      // per <= 4 since depth <= 14
+      double v[8];
+      // per <= 8 since depth <= 15
       for (int j = 0; j < per; ++j) v[j] = sums[i * per + j];
-      if (per == 2) v[0] = __dadd_rn(v[0], v[1]);
-      if (per == 4) v[0] = __dadd_rn(__dadd_rn(v[0], v[1]), __dadd_rn(v[2], v[3]));
+      for (int w = per; w > 1; w >>= 1)  // levels of the perfect binary tree, bottom up
+        for (int j = 0; j < w / 2; ++j) v[j] = __dadd_rn(v[2 * j], v[2 * j + 1]);
       buf[i] = v[0];
     }
   } else {
