@@ -279,14 +279,20 @@ def plan_microbatches(traj_bounds: torch.Tensor, item_traj: torch.Tensor, mb_off
             raise ValueError(f"item_traj has {item_traj.numel()} entries, needs {n_items}")
     else:
         mb_off_d, mb_tok_d = _upload([mb_offsets, mb_token_start], dev)
+    # two allocations sliced into the plan's outputs (every entry is written by K4,
+    # status included: no memset)
+    m1 = max(M, 1)
+    b32 = torch.empty(4 * n_items + M + 2 * m1, **i32)
+    b64 = torch.empty(2 * n_items + M + 1, dtype=torch.int64, device=dev)
+    o = np.cumsum([0, n_items, n_items, n_items, n_items + M, m1, m1])
     plan = DevicePlan(
-        group_of=torch.empty(n_items, **i32), slot_of=torch.empty(n_items, **i32),
-        n_groups=torch.empty(max(M, 1), **i32),
-        group_cu=torch.empty(n_items + M, dtype=torch.int64, device=dev),
-        group_seq_cu=torch.empty(n_items + M, **i32), packed_traj=torch.empty(n_items, **i32),
-        seq_cu=torch.empty(n_items + 1, dtype=torch.int64, device=dev),
-        status=torch.zeros(max(M, 1), **i32), mb_offsets=mb_offsets,
-        mb_token_start=mb_token_start, n_packed_tokens=0)
+        group_of=b32[o[0]:o[1]], slot_of=b32[o[1]:o[2]], packed_traj=b32[o[2]:o[3]],
+        group_seq_cu=b32[o[3]:o[4]], n_groups=b32[o[4]:o[5]], status=b32[o[5]:o[6]],
+        group_cu=b64[:n_items + M], seq_cu=b64[n_items + M:],
+        mb_offsets=mb_offsets, mb_token_start=mb_token_start, n_packed_tokens=0)
+    if M == 0:  # nothing for K4 to write
+        b32.zero_()
+        b64.zero_()
     check(lib.areal_plan_microbatches(
         _ptr(traj_bounds), _ptr(item_traj), _ptr(mb_off_d), _ptr(mb_tok_d), M, n_items, max_items,
         int(capacity), int(min_groups), _ptr(plan.group_of), _ptr(plan.slot_of),
