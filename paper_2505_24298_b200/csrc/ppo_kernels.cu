@@ -406,9 +406,9 @@ __device__ __forceinline__ void rowcta_fold(RowStat<A>& rs, const A (&f)[E]) {
   }
 }
 
-template <typename T, bool BWD, bool ENT>
+template <typename T, bool BWD, bool ENT, int NT = RowCtaGeo<BWD>::kThreads>
 __device__ __forceinline__ void row_cta_body(const PpoArgs& a) {
-  constexpr int kRowCtaThreads = RowCtaGeo<BWD>::kThreads;
+  constexpr int kRowCtaThreads = NT;
   using A = typename Traits<T>::Acc;
   constexpr int E = Vec<T>::N;
   using U = typename std::conditional<std::is_same<T, double>::value, double, float>::type;
@@ -564,6 +564,12 @@ template <typename T, bool ENT>
 __global__ void __launch_bounds__(RowCtaGeo<true>::kThreads, RowCtaGeo<true>::kBlocks)
     ppo_rowcta_kernel(PpoArgs a) {
   row_cta_body<T, true, ENT>(a);
+}
+// K2 on short rows (<= 32 KB): 8 x 256 threads per SM, like K1 — the rows in flight
+// still fit L2 and the per-row epilogues overlap across 8 CTAs.
+template <typename T, bool ENT>
+__global__ void __launch_bounds__(256, 8) ppo_rowcta_small_kernel(PpoArgs a) {
+  row_cta_body<T, true, ENT, 256>(a);
 }
 
 
@@ -778,8 +784,15 @@ static int launch_warp(PpoArgs a, cudaStream_t stream) {
 }
 
 template <typename T, bool BWD>
-static int launch_rowcta(PpoArgs a, cudaStream_t stream) {
+static int launch_rowcta(PpoArgs a, cudaStream_t stream, bool small = false) {
   DevInfo d = get_dev();
+  if (BWD && small) {
+    const int64_t grid = std::min<int64_t>(a.n_rows, (int64_t)d.sms * 8);
+    auto kern = a.ent_out ? ppo_rowcta_small_kernel<T, true> : ppo_rowcta_small_kernel<T, false>;
+    kern<<<(unsigned)grid, 256, 0, stream>>>(a);
+    AREAL_CUDA_CHECK_LAUNCH();
+    return AREAL_OK;
+  }
   const int64_t grid = std::min<int64_t>(a.n_rows, (int64_t)d.sms * RowCtaGeo<BWD>::kBlocks);
   auto kern = a.ent_out ? (BWD ? ppo_rowcta_kernel<T, true> : logprob_rowcta_kernel<T, true>)
                         : (BWD ? ppo_rowcta_kernel<T, false> : logprob_rowcta_kernel<T, false>);
@@ -825,6 +838,14 @@ static bool k1_unal_off() {  // AREAL_K1_RING_UNALIGNED=0: unaligned K1 rows on 
   return off;
 }
 
+static int64_t small_rowcta_kb() {  // K2 rows up to this many KB on the short-row kernel
+  static const int64_t kb = [] {
+    const char* s = getenv("AREAL_K2_SMALL_ROWCTA_KB");  // -1 / unset: the default rule
+    return s ? (int64_t)atoi(s) : (int64_t)-1;
+  }();
+  return kb;
+}
+
 static bool rowcta_off() {  // AREAL_ROWCTA=0: unaligned rows on the one-warp kernel
   static const bool off = [] {
     const char* s = getenv("AREAL_ROWCTA");
@@ -844,6 +865,20 @@ static int dispatch(PpoArgs a, int dtype, int algo, cudaStream_t stream) {
     ring = true;
   } else if (algo == AREAL_ALGO_AUTO) {
     ring = aligned && a.vocab * es >= 16384;
+  }
+  // short K2 rows: one CTA per row, 8 per SM (beats the TMEM / ring / one-warp
+  // kernels up to 16 KB rows, and fp32 rows up to 32 KB; profiles/r01_k2_small_rows_tmem.txt)
+  const int64_t small_kb = small_rowcta_kb();
+  const int64_t small_lim = small_kb >= 0 ? small_kb * 1024 : (es == 4 ? 32768 : 16384);
+  const bool small_row = a.vocab * es <= small_lim && a.vocab >= 256 && es <= 4;  // fp64: one-warp kernel
+  if (BWD && small_row && algo == AREAL_ALGO_AUTO) {
+    switch (dtype) {
+      case AREAL_F32: return launch_rowcta<float, BWD>(a, stream, true);
+      case AREAL_BF16: return launch_rowcta<__nv_bfloat16, BWD>(a, stream, true);
+      case AREAL_F16: return launch_rowcta<__half, BWD>(a, stream, true);
+      case AREAL_F64: return launch_rowcta<double, BWD>(a, stream, true);
+      default: return AREAL_ERR_BAD_DTYPE;
+    }
   }
   if (ring) {
     int rc;
@@ -892,10 +927,10 @@ static int dispatch(PpoArgs a, int dtype, int algo, cudaStream_t stream) {
   // unaligned (or ring-refused) rows of >= 16 KB: one CTA per row, body in 16-byte vectors
   if (algo == AREAL_ALGO_AUTO && a.vocab * es >= 16384 && !rowcta_off()) {
     switch (dtype) {
-      case AREAL_F32: return launch_rowcta<float, BWD>(a, stream);
-      case AREAL_BF16: return launch_rowcta<__nv_bfloat16, BWD>(a, stream);
-      case AREAL_F16: return launch_rowcta<__half, BWD>(a, stream);
-      case AREAL_F64: return launch_rowcta<double, BWD>(a, stream);
+      case AREAL_F32: return launch_rowcta<float, BWD>(a, stream, small_row);
+      case AREAL_BF16: return launch_rowcta<__nv_bfloat16, BWD>(a, stream, small_row);
+      case AREAL_F16: return launch_rowcta<__half, BWD>(a, stream, small_row);
+      case AREAL_F64: return launch_rowcta<double, BWD>(a, stream, small_row);
       default: return AREAL_ERR_BAD_DTYPE;
     }
   }
