@@ -66,8 +66,9 @@ typedef enum { AREAL_F32 = 0, AREAL_BF16 = 1, AREAL_F16 = 2, AREAL_F64 = 3 } are
  * split) and all of K1 -> ROW_RING (TMA bulk ring).  Unaligned rows of >= 16 KB:
  * K2 on 16/32-bit rows -> the TMEM kernel (masked 16-byte-aligned loads) when dlogits
  * share the logits' 16-byte phase; K1 on long rows -> the ring kernel (masked
- * 16-byte-aligned loads); otherwise one CTA per row; rows under 16 KB -> ROW_WARP
- * (one warp per row).  ROW_RING /
+ * 16-byte-aligned loads); otherwise one CTA per row.  Short K2 rows (<= 16 KB of
+ * 16-bit, <= 32 KB of fp32 logits) -> one CTA per row, 8 per SM; other rows under
+ * 16 KB (all of K1, fp64 K2) -> ROW_WARP (one warp per row).  ROW_RING /
  * ROW_WARP force the respective family. */
 typedef enum { AREAL_ALGO_AUTO = 0, AREAL_ALGO_ROW_WARP = 1, AREAL_ALGO_ROW_RING = 2 } areal_algo_t;
 

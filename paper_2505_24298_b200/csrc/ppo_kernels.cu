@@ -7,7 +7,8 @@
 //
 // Kernels (AREAL_ALGO_AUTO picks per shape):
 //   row_warp : one warp per row, any vocab / alignment; both passes read global
-//              memory (the second pass hits L1/L2).  Rows under 16 KB.
+//              memory (the second pass hits L1/L2).  K1 rows under 16 KB, fp64 K2.
+//   row_cta_small : K2 rows <= 16 KB (16-bit) / 32 KB (fp32), one CTA per row, 8 per SM.
 //   row_cta  : one CTA per row for rows >= 16 KB that are not 16-byte aligned
 //              (scalar head / 16-byte-vector body / scalar tail; K2 re-reads from L2):
 //              shorter K1 rows and K2 rows the TMEM kernel cannot take (long unaligned
