@@ -277,16 +277,50 @@ __device__ __forceinline__ void row_warp_body(const PpoArgs& a) {
     const int64_t tok = a.tokens[idx];
     RowStat<A> rs;
     rs.init();
-    for (int64_t base = 0; base < V; base += 32 * kWarpUnroll) {
-      A v[kWarpUnroll];
-      A lmax = Lim<A>::ninf();
+    if (!BWD && sizeof(T) <= 4 && (((uintptr_t)x | (uintptr_t)(V * (int64_t)sizeof(T))) & 15) == 0) {
+      // K1, 16-byte-aligned row of 16/32-bit logits: 16-byte vector loads, 4 per lane
+      // in flight (bf16 V = 4,096: 2.87 -> 4.87 TB/s).  fp64 keeps the 8-deep scalar
+      // fold (its rescale exp amortised over 8 values, not 2); the K2 warp path (fp64
+      // rows, forced algo) keeps the scalar fold too.
+      constexpr int E = Vec<T>::N, U = 4;
+      using Un = typename std::conditional<std::is_same<T, double>::value, double, float>::type;
+      const uint4* xv = reinterpret_cast<const uint4*>(x);
+      const int64_t nv = V * (int64_t)sizeof(T) / 16;
+      for (int64_t base = 0; base < nv; base += 32 * U) {
+        uint4 q[U];
 #pragma unroll
-      for (int u = 0; u < kWarpUnroll; ++u) {
-        const int64_t i = base + u * 32 + lane;
-        v[u] = (i < V) ? Traits<T>::to_acc(x[i]) : Lim<A>::ninf();
-        lmax = fmax(lmax, v[u]);
+        for (int u = 0; u < U; ++u) {
+          const int64_t i = base + u * 32 + lane;
+          q[u] = i < nv ? xv[i] : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (base + u * 32 + lane < nv) {
+            Un g[E];
+            Vec<T>::unpack(q[u], g);
+            A v[E];
+            A lmax = Lim<A>::ninf();
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+              v[e] = (A)g[e];
+              lmax = fmax(lmax, v[e]);
+            }
+            fold(rs, v, lmax);
+          }
+        }
       }
-      fold(rs, v, lmax);
+    } else {
+      for (int64_t base = 0; base < V; base += 32 * kWarpUnroll) {
+        A v[kWarpUnroll];
+        A lmax = Lim<A>::ninf();
+#pragma unroll
+        for (int u = 0; u < kWarpUnroll; ++u) {
+          const int64_t i = base + u * 32 + lane;
+          v[u] = (i < V) ? Traits<T>::to_acc(x[i]) : Lim<A>::ninf();
+          lmax = fmax(lmax, v[u]);
+        }
+        fold(rs, v, lmax);
+      }
     }
     rs.warp_reduce();
     const A lse_s = Ex<A>::lse_shift(rs.m == Lim<A>::ninf() ? A(0) : rs.m, rs.s);
