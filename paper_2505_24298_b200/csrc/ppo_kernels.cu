@@ -168,7 +168,10 @@ __device__ __forceinline__ void fold(RowStat<A>& rs, const A (&v)[N], A lmax) {
   const A mn = fmax(rs.m, lmax);
   const A muse = (mn == Lim<A>::ninf()) ? A(0) : mn;
   const A c = Ex<A>::shift(muse);
-  const A r = Ex<A>::e(rs.m, c);  // rescale of the old partial sums (0 when m = -inf)
+  // rescale of the old partial sums (0 when m = -inf); exactly 1 when the max did not
+  // move — Ex::e(m, shift(m)) is 2^(rounding residual), a same-signed bias that would
+  // compound over the row's fold calls
+  const A r = mn == rs.m ? A(1) : Ex<A>::e(rs.m, c);
   A s = rs.s * r, sx = rs.sx * r;
 #pragma unroll
   for (int i = 0; i < N; ++i) {
@@ -277,11 +280,9 @@ __device__ __forceinline__ void row_warp_body(const PpoArgs& a) {
     const int64_t tok = a.tokens[idx];
     RowStat<A> rs;
     rs.init();
-    if (!BWD && sizeof(T) <= 4 && (((uintptr_t)x | (uintptr_t)(V * (int64_t)sizeof(T))) & 15) == 0) {
-      // K1, 16-byte-aligned row of 16/32-bit logits: 16-byte vector loads, 4 per lane
-      // in flight (bf16 V = 4,096: 2.87 -> 4.87 TB/s).  fp64 keeps the 8-deep scalar
-      // fold (its rescale exp amortised over 8 values, not 2); the K2 warp path (fp64
-      // rows, forced algo) keeps the scalar fold too.
+    if (sizeof(T) <= 4 && (((uintptr_t)x | (uintptr_t)(V * (int64_t)sizeof(T))) & 15) == 0) {
+      // 16-byte-aligned row of 16/32-bit logits: 16-byte vector loads, 4 per lane in
+      // flight (bf16 V = 4,096: 2.87 -> 4.87 TB/s).  fp64 keeps the 8-deep scalar fold.
       constexpr int E = Vec<T>::N, U = 4;
       using Un = typename std::conditional<std::is_same<T, double>::value, double, float>::type;
       const uint4* xv = reinterpret_cast<const uint4*>(x);

@@ -241,7 +241,8 @@ __device__ __forceinline__ void fold_values(RowStat<typename Traits<T>::Acc>& rs
   const A mn = fmax(rs.m, lmax);
   const A muse = (mn == Lim<A>::ninf()) ? A(0) : mn;
   const A c = Ex<A>::shift(muse);
-  const A r = need_max ? Ex<A>::e(rs.m, c) : A(1);  // rescale of the running sums (0 while m = -inf)
+  // rescale of the running sums (0 while m = -inf; exactly 1 when the max did not move)
+  const A r = (need_max && mn != rs.m) ? Ex<A>::e(rs.m, c) : A(1);
   if constexpr (std::is_same<A, float>::value) {
     const float2 L2 = make_float2(Lim<float>::kLog2e, Lim<float>::kLog2e);
     const float2 C2 = make_float2(-c, -c);
