@@ -391,7 +391,8 @@ __global__ void __launch_bounds__(THREADS, 1)
           for (int i = 1; i < 32; ++i) lmax = fmaxf(lmax, cv[i]);
           const float mn = fmaxf(m, lmax);
           const float c = (mn == -INFINITY) ? 0.f : mn * L2E;
-          const float r = fast_exp2(fmaf(m, L2E, -c));
+          // exactly 1 while the max stays (2^(rounding residual) would compound)
+          const float r = (m == mn) ? 1.f : fast_exp2(fmaf(m, L2E, -c));
           const float2 L2 = make_float2(L2E, L2E), C2 = make_float2(-c, -c);
           float2 s2 = make_float2(0.f, 0.f), x2 = make_float2(0.f, 0.f);
 #pragma unroll
