@@ -280,13 +280,22 @@ __device__ __forceinline__ void row_warp_body(const PpoArgs& a) {
     const int64_t tok = a.tokens[idx];
     RowStat<A> rs;
     rs.init();
-    if (sizeof(T) <= 4 && (((uintptr_t)x | (uintptr_t)(V * (int64_t)sizeof(T))) & 15) == 0) {
-      // 16-byte-aligned row of 16/32-bit logits: 16-byte vector loads, 4 per lane in
-      // flight (bf16 V = 4,096: 2.87 -> 4.87 TB/s).  fp64 keeps the 8-deep scalar fold.
+    if (sizeof(T) <= 4) {
+      // 16/32-bit logits: scalar head up to the first 16-byte boundary, 16-byte vector
+      // body (4 loads per lane in flight), scalar tail (bf16 V = 4,096: 2.87 -> 4.87
+      // TB/s).  fp64 keeps the 8-deep scalar fold below.
       constexpr int E = Vec<T>::N, U = 4;
       using Un = typename std::conditional<std::is_same<T, double>::value, double, float>::type;
-      const uint4* xv = reinterpret_cast<const uint4*>(x);
-      const int64_t nv = V * (int64_t)sizeof(T) / 16;
+      int64_t nh = (int64_t)(((16 - ((uintptr_t)x & 15)) & 15) / sizeof(T));
+      if (nh > V) nh = V;
+      const uint4* xv = reinterpret_cast<const uint4*>(x + nh);
+      const int64_t nv = (V - nh) / E;
+      const int64_t t0 = nh + nv * E;
+      for (int64_t i = lane; i < nh + (V - t0); i += 32) {  // head and tail elements
+        const int64_t k = i < nh ? i : t0 + (i - nh);
+        const A v1[1] = {Traits<T>::to_acc(x[k])};
+        fold(rs, v1, v1[0]);
+      }
       for (int64_t base = 0; base < nv; base += 32 * U) {
         uint4 q[U];
 #pragma unroll
