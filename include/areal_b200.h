@@ -126,7 +126,15 @@ size_t areal_workspace_bytes(void);
  * Replaces recompute_prox_logprobs (trainer.py:128-137) ->
  * batch_token_log_probs (policy.py:159-163) -> log_softmax (policy.py:145-147)
  * on given logits.  lp_out[idx] = x_r[a] - logsumexp(x_r); entropy_out may be
- * NULL.  Reads each logits row once. */
+ * NULL.  Reads each logits row once.
+ *
+ * Memory precondition (K1 and K2): rows whose start is not 16-byte aligned are
+ * streamed with 16-byte bulk copies from the 16-byte boundary at or below each
+ * row start to the boundary at or above its end, so the first and last row may
+ * read up to 15 bytes outside [logits, logits + n_rows * ld_logits * size).  The
+ * bytes are masked and never affect results; a 16-byte granule never crosses a
+ * page, so the over-read cannot fault on any CUDA allocation.  Rows that start
+ * on a 16-byte boundary with a 16-byte multiple length never over-read. */
 int areal_logprob_fwd(const void* logits, int64_t ld_logits, int dtype, int64_t n_rows,
                       int64_t vocab, const int64_t* tokens, const int32_t* row_index,
                       double* lp_out, double* entropy_out, int algo,

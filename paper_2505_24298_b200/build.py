@@ -65,25 +65,44 @@ def build_packer(force: bool = False) -> str:
     return out
 
 
-def build(verbose: bool = False, force: bool = False, extra_flags=()) -> str:
+def build(verbose: bool = False, force: bool = False, extra_flags=(), out: str | None = None) -> str:
+    """Compile every translation unit in parallel (one nvcc per source), then link."""
+    from concurrent.futures import ThreadPoolExecutor
+    import tempfile
     build_packer(force=force)
-    if not force and not _stale():
+    out = out or LIB_PATH
+    if out == LIB_PATH and not force and not _stale():
         return LIB_PATH
-    cmd = [nvcc_path(), *ARCH, "-O3", "-std=c++17", "-lineinfo", "--expt-relaxed-constexpr",
-           "-Xcompiler", "-fPIC", "-shared", "-cudart", "shared", "-Xlinker", "-rpath,/usr/local/cuda/lib64",
-           "-I", os.path.join(ROOT, "include"), *extra_flags]
+    nvcc = nvcc_path()
+    common = [*ARCH, "-O3", "-std=c++17", "-lineinfo", "--expt-relaxed-constexpr",
+              "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"), *extra_flags]
     if verbose:
-        cmd += ["-Xptxas", "-v"]
-    cmd += [os.path.join(CSRC, s) for s in SOURCES]
-    tmp = LIB_PATH + ".tmp"
-    cmd += ["-o", tmp]
-    res = subprocess.run(cmd, capture_output=True, text=True)
+        common += ["-Xptxas", "-v"]
+    tmpdir = tempfile.mkdtemp(prefix="areal_build_")
+
+    def compile_one(src):
+        obj = os.path.join(tmpdir, os.path.splitext(src)[0] + ".o")
+        cmd = [nvcc, *common, "-c", os.path.join(CSRC, src), "-o", obj]
+        return cmd, subprocess.run(cmd, capture_output=True, text=True), obj
+
+    with ThreadPoolExecutor(len(SOURCES)) as ex:
+        results = list(ex.map(compile_one, SOURCES))
+    logs = []
+    for cmd, res, _ in results:
+        if res.returncode != 0:
+            raise RuntimeError(f"nvcc failed ({res.returncode}):\n{' '.join(cmd)}\n{res.stdout}\n{res.stderr}")
+        logs.append(res.stdout + res.stderr)
+    tmp = out + ".tmp"
+    link = [nvcc, *ARCH, "-shared", "-cudart", "shared", "-Xlinker", "-rpath,/usr/local/cuda/lib64",
+            *[obj for _, _, obj in results], "-o", tmp]
+    res = subprocess.run(link, capture_output=True, text=True)
+    shutil.rmtree(tmpdir, ignore_errors=True)
     if res.returncode != 0:
-        raise RuntimeError(f"nvcc failed ({res.returncode}):\n{' '.join(cmd)}\n{res.stdout}\n{res.stderr}")
+        raise RuntimeError(f"nvcc link failed ({res.returncode}):\n{' '.join(link)}\n{res.stdout}\n{res.stderr}")
     if verbose:
-        sys.stderr.write(res.stdout + res.stderr)
-    os.replace(tmp, LIB_PATH)
-    return LIB_PATH
+        sys.stderr.write("".join(logs))
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":

@@ -5,6 +5,7 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <stdint.h>
+#include <type_traits>
 
 #include "../../include/areal_b200.h"
 
@@ -87,8 +88,17 @@ template <typename A> struct RowStat {
   __device__ __forceinline__ void merge(A m2, A s2, A sx2) {
     A mn = fmax(m, m2);
     if (mn == Lim<A>::ninf()) return;  // both empty / all -inf
-    A a = fast_exp2((m - mn) * Lim<A>::kLog2e);
-    A b = fast_exp2((m2 - mn) * Lim<A>::kLog2e);
+    A a, b;
+    if constexpr (std::is_same<A, float>::value) {
+      // fp32 partials are sums of 2^(x log2e - fl(m log2e)): move them to the new
+      // shift by the exact 2^(fl(m log2e) - fl(mn log2e)) (no FMA contraction)
+      const float cn = __fmul_rn(mn, Lim<A>::kLog2e);
+      a = fast_exp2(__fmul_rn(m, Lim<A>::kLog2e) - cn);
+      b = fast_exp2(__fmul_rn(m2, Lim<A>::kLog2e) - cn);
+    } else {
+      a = fast_exp2((m - mn) * Lim<A>::kLog2e);
+      b = fast_exp2((m2 - mn) * Lim<A>::kLog2e);
+    }
     s = s * a + s2 * b;
     sx = sx * a + sx2 * b;
     m = mn;
@@ -331,7 +341,8 @@ namespace areal {
 // nearest integer (1.5*2^23 rounding trick), 2^f by a degree-3 fit on [-0.5, 0.5]
 // (max relative error 7.5e-5: only for 16-bit outputs), 2^n added to the exponent
 // bits with one IMAD.  Arguments below -126 are clamped (result ~1e-38, vs 0).
-__device__ __forceinline__ float2 exp2_poly3(float2 x) {
+__device__ __forceinline__ float2 exp2_poly3(float2 x_in) {
+  float2 x = x_in;
   // clamp to [-126, 129]: from ~128.5 the exponent add overflows into inf/NaN bits, so an
   // overflowing argument still yields a non-finite value (detected by the fixed-shift
   // folds) instead of a wrapped finite one
@@ -344,7 +355,10 @@ __device__ __forceinline__ float2 exp2_poly3(float2 x) {
                    make_float2(0.2426111400127411f, 0.2426111400127411f));
   p = ffma2(p, f, make_float2(0.6932609677314758f, 0.6932609677314758f));
   p = ffma2(p, f, make_float2(0.9999280571937561f, 0.9999280571937561f));
-  return make_float2(__int_as_float(__float_as_int(t.x) * (1 << 23) + __float_as_int(p.x)),
-                     __int_as_float(__float_as_int(t.y) * (1 << 23) + __float_as_int(p.y)));
+  // the clamp's fmaxf would turn a NaN argument into -126 (a silent ~0): a NaN logit
+  // must poison the row's sum as on the MUFU path, so NaN arguments pass through
+  const float rx = __int_as_float(__float_as_int(t.x) * (1 << 23) + __float_as_int(p.x));
+  const float ry = __int_as_float(__float_as_int(t.y) * (1 << 23) + __float_as_int(p.y));
+  return make_float2(x_in.x == x_in.x ? rx : x_in.x, x_in.y == x_in.y ? ry : x_in.y);
 }
 }  // namespace areal

@@ -392,7 +392,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           const float mn = fmaxf(m, lmax);
           const float c = (mn == -INFINITY) ? 0.f : mn * L2E;
           // exactly 1 while the max stays (2^(rounding residual) would compound)
-          const float r = (m == mn) ? 1.f : fast_exp2(fmaf(m, L2E, -c));
+          const float r = (m == mn) ? 1.f : fast_exp2(__fmul_rn(m, L2E) - c);  // 2^(c_old - c_new), no FMA contraction
           const float2 L2 = make_float2(L2E, L2E), C2 = make_float2(-c, -c);
           float2 s2 = make_float2(0.f, 0.f), x2 = make_float2(0.f, 0.f);
 #pragma unroll

@@ -147,6 +147,12 @@ template <> struct Ex<float> {
   static __device__ __forceinline__ float e(float x, float c) {
     return fast_exp2(fmaf(x, Lim<float>::kLog2e, -c));
   }
+  // factor taking sums accumulated against shift(m_old) to the new shift c: the exact
+  // 2^(shift(m_old) - c) (0 when m_old = -inf), not e(m_old, c), which would carry the
+  // old shift's rounding residual into every max move
+  static __device__ __forceinline__ float rescale(float m_old, float c) {
+    return fast_exp2(__fmul_rn(m_old, Lim<float>::kLog2e) - c);
+  }
   // lse in "shift units" (log2 domain) from (m, s)
   static __device__ __forceinline__ float lse_shift(float m, float s) {
     return m * Lim<float>::kLog2e + __log2f(s);
@@ -158,6 +164,7 @@ template <> struct Ex<float> {
 template <> struct Ex<double> {
   static __device__ __forceinline__ double shift(double m) { return m; }
   static __device__ __forceinline__ double e(double x, double c) { return exp(x - c); }
+  static __device__ __forceinline__ double rescale(double m_old, double c) { return exp(m_old - c); }
   static __device__ __forceinline__ double lse_shift(double m, double s) { return m + log(s); }
   static __device__ __forceinline__ double lse_nat(double l) { return l; }
 };
@@ -171,7 +178,7 @@ __device__ __forceinline__ void fold(RowStat<A>& rs, const A (&v)[N], A lmax) {
   // rescale of the old partial sums (0 when m = -inf); exactly 1 when the max did not
   // move — Ex::e(m, shift(m)) is 2^(rounding residual), a same-signed bias that would
   // compound over the row's fold calls
-  const A r = mn == rs.m ? A(1) : Ex<A>::e(rs.m, c);
+  const A r = mn == rs.m ? A(1) : Ex<A>::rescale(rs.m, c);
   A s = rs.s * r, sx = rs.sx * r;
 #pragma unroll
   for (int i = 0; i < N; ++i) {
@@ -425,7 +432,8 @@ __device__ __forceinline__ void rowcta_fold(RowStat<A>& rs, const A (&f)[E]) {
   for (int e = 1; e < E; ++e) lmax = fmax(lmax, f[e]);
   if constexpr (std::is_same<A, float>::value && E % 2 == 0) {
     if (lmax > rs.m) {
-      const float r = rs.m == Lim<float>::ninf() ? 0.f : fast_exp2((rs.m - lmax) * Lim<float>::kLog2e);
+      const float r = rs.m == Lim<float>::ninf() ? 0.f
+          : fast_exp2(__fmul_rn(rs.m, Lim<float>::kLog2e) - __fmul_rn(lmax, Lim<float>::kLog2e));
       rs.s *= r;
       if (ENT) rs.sx *= r;
       rs.m = lmax;

@@ -242,7 +242,7 @@ __device__ __forceinline__ void fold_values(RowStat<typename Traits<T>::Acc>& rs
   const A muse = (mn == Lim<A>::ninf()) ? A(0) : mn;
   const A c = Ex<A>::shift(muse);
   // rescale of the running sums (0 while m = -inf; exactly 1 when the max did not move)
-  const A r = (need_max && mn != rs.m) ? Ex<A>::e(rs.m, c) : A(1);
+  const A r = (need_max && mn != rs.m) ? Ex<A>::rescale(rs.m, c) : A(1);
   if constexpr (std::is_same<A, float>::value) {
     const float2 L2 = make_float2(Lim<float>::kLog2e, Lim<float>::kLog2e);
     const float2 C2 = make_float2(-c, -c);
@@ -294,7 +294,7 @@ template <typename A, bool ENT>
 __device__ __forceinline__ RowStat<A> warp_merge_ent(const RowStat<A>& w) {
   const A M = warp_max(w.m);
   const A muse = (M == Lim<A>::ninf()) ? A(0) : M;
-  const A f = (w.m == Lim<A>::ninf()) ? A(0) : Ex<A>::e(w.m, Ex<A>::shift(muse));
+  const A f = (w.m == Lim<A>::ninf()) ? A(0) : Ex<A>::rescale(w.m, Ex<A>::shift(muse));
   A s = w.s * f, sx = ENT ? w.sx * f : A(0);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {

@@ -288,7 +288,7 @@ __device__ __forceinline__ float fold_to_e(RowStat<float>& rs, uint32_t (&w)[kTW
   const float mn = fmaxf(rs.m, lmax);
   const float muse = (mn == Lim<float>::ninf()) ? 0.f : mn;
   const float c = Ex<float>::shift(muse);
-  const float r = need_max ? Ex<float>::e(rs.m, c) : 1.f;
+  const float r = (need_max && mn != rs.m) ? Ex<float>::rescale(rs.m, c) : 1.f;
   const float2 L2 = make_float2(Lim<float>::kLog2e, Lim<float>::kLog2e);
   const float2 C2 = make_float2(-c, -c);
   float2 s2 = make_float2(0.f, 0.f), x2 = make_float2(0.f, 0.f);

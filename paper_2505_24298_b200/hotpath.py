@@ -33,7 +33,7 @@ import torch
 import torch.distributed as dist
 
 from . import kernels as K
-from .trainer import BatchError, minibatch_items, _status_error
+from .trainer import BatchError, minibatch_items, _status_error, _check_items, _device_capacity
 
 ADV_NORM_ALIASES = {"group": "group_token"}
 
@@ -276,8 +276,11 @@ class DecoupledPPOStep:
         mb_tokens = [int(lens[x].sum()) for x in items]
         mb_token_start = np.concatenate([[0], np.cumsum(mb_tokens)[:-1]]).astype(np.int64)
         flat = np.concatenate(items).astype(np.int32)  # staged with the offsets, one copy
+        cap = c.micro_token_budget
+        if max(int(lens[x].max()) for x in items) <= cap:  # else K4 reports the bad length
+            _check_items(max(len(x) for x in items))
         dplan = K.plan_microbatches(ro.traj_bounds, flat, mb_offsets, mb_token_start,
-                                    c.micro_token_budget, c.micro_min_groups)
+                                    _device_capacity(cap, [max(mb_tokens)]), c.micro_min_groups)
         # the single host read of the plan: micro-batch sizes drive the model's shapes
         M, n_gc = len(items), dplan.group_cu.numel()
         need = 16 * M + 8 * n_gc

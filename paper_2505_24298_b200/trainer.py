@@ -214,11 +214,22 @@ def _linear_logits(X: torch.Tensor, W: torch.Tensor, b: torch.Tensor) -> torch.T
     return torch.addmm(b, X, W.t())
 
 
-def _adv_kwargs(config: TrainerConfig | None):
-    if config is None:
-        return dict(mode="reference", norm="global")
-    norm = {"group": "group_token"}.get(config.adv_norm, config.adv_norm)
-    return dict(mode=config.adv_mode, gamma=config.gamma, lam=config.lam, norm=norm)
+# Extension fields of TrainerConfig and the values that reproduce the reference.  The
+# reference's own asyncrl.trainer.TrainerConfig (trainer.py:38-53) has none of them, so
+# every read goes through _ext: either config class drives this module unchanged.
+_EXT_DEFAULTS = dict(eta_mask=-1, behav_weight_cap=0.0, adv_mode="reference", gamma=1.0,
+                     lam=1.0, adv_norm="global")
+
+
+def _ext(config, name):
+    return _EXT_DEFAULTS[name] if config is None else getattr(config, name, _EXT_DEFAULTS[name])
+
+
+def _adv_kwargs(config):
+    norm = _ext(config, "adv_norm")
+    norm = {"group": "group_token"}.get(norm, norm)
+    return dict(mode=_ext(config, "adv_mode"), gamma=_ext(config, "gamma"),
+                lam=_ext(config, "lam"), norm=norm)
 
 
 def _advantages_device(batch, dev, config=None) -> torch.Tensor:
@@ -360,6 +371,30 @@ def _status_error(code: int, lengths, capacity) -> BatchError:
     return BatchError(f"allocation failed with status {code}")
 
 
+_INT32_MAX = 2 ** 31 - 1
+
+
+def _device_capacity(capacity, lengths) -> int:
+    """K4 takes an int32 capacity.  A capacity at or above the total length admits every
+    placement (totals[g] + s never exceeds the sum of distinct lengths), so larger
+    values are clamped to the total with identical groups (trainer.py:258)."""
+    capacity = int(capacity)
+    if capacity > _INT32_MAX:
+        capacity = max(int(sum(lengths)), 1)
+        if capacity > _INT32_MAX:
+            raise BatchError(f"minibatch of {capacity} tokens exceeds the GPU allocator's "
+                             f"int32 token range")
+    return capacity
+
+
+def _check_items(n_items: int) -> None:
+    from ._lib import MAX_ITEMS_PER_MINIBATCH
+    if n_items > MAX_ITEMS_PER_MINIBATCH:
+        raise BatchError(f"{n_items} sequences in one minibatch exceed the GPU allocator's "
+                         f"limit of {MAX_ITEMS_PER_MINIBATCH} (split the batch into more "
+                         f"minibatches)")
+
+
 def allocate_microbatches(lengths, capacity: int, min_groups: int = 1) -> MicrobatchPlan:
     """trainer.py:235-270 on the GPU (K4), bit-exact group assignment."""
     lengths = [int(s) for s in lengths]
@@ -368,11 +403,14 @@ def allocate_microbatches(lengths, capacity: int, min_groups: int = 1) -> Microb
     if not lengths:
         return MicrobatchPlan(groups=(), capacity=capacity, min_groups=min_groups)
     dev = _device()
+    if 1 <= min(lengths) and max(lengths) <= capacity:  # else the device reports the
+        _check_items(len(lengths))                          # first bad length (248-252)
+    cap = _device_capacity(capacity, [max(s, 0) for s in lengths])
     bounds = np.concatenate([[0], np.cumsum(lengths)]).astype(np.int64)
     # the device validates lengths and reports the first failing item (trainer.py:248-252)
     plan = K.plan_microbatches(_d(bounds, torch.int64, dev),
                                torch.arange(len(lengths), dtype=torch.int32, device=dev),
-                               [0, len(lengths)], [0], capacity, min_groups)
+                               [0, len(lengths)], [0], cap, min_groups)
     status = int(plan.status[0].item())
     if status != 0:
         raise _status_error(status, lengths, capacity)
@@ -432,6 +470,9 @@ def plan_step(bounds_host: np.ndarray, bounds_dev: torch.Tensor, minibatches: in
     lens = np.diff(bounds_host)
     mb_tokens = [int(lens[x].sum()) for x in items]
     mb_token_start = np.concatenate([[0], np.cumsum(mb_tokens)[:-1]]).astype(np.int64)
+    if max(int(lens[x].max()) for x in items) <= capacity:  # else K4 reports the bad length
+        _check_items(max(len(x) for x in items))
+    capacity = _device_capacity(capacity, [max(mb_tokens)])
     flat = torch.as_tensor(np.concatenate(items).astype(np.int32)).to(dev)
     plan = K.plan_microbatches(bounds_dev, flat, mb_offsets, mb_token_start, capacity, min_groups)
     n_packed = int(sum(mb_tokens))
@@ -450,6 +491,7 @@ class _DeviceAdam:
 
     def __init__(self, opt, dev):
         self.opt = opt
+        self.step_count = int(opt.step)  # committed to opt with the moments (write_back)
         self.m_w = _d(opt.m_weights, torch.float64, dev)
         self.v_w = _d(opt.v_weights, torch.float64, dev)
         self.m_b = _d(opt.m_bias, torch.float64, dev)
@@ -458,19 +500,23 @@ class _DeviceAdam:
     def step(self, W, b, gw, gb, cfg, grad_scale=1.0):
         """W, b are updated in place; gw, gb are the raw (unscaled) gradient sums."""
         norm = K.adam_step([W, b], [gw, gb], [self.m_w, self.m_b], [self.v_w, self.v_b],
-                           step=self.opt.step + 1, lr=cfg.lr, beta1=cfg.beta1, beta2=cfg.beta2,
+                           step=self.step_count + 1, lr=cfg.lr, beta1=cfg.beta1, beta2=cfg.beta2,
                            eps=cfg.eps, weight_decay=cfg.weight_decay, clip_norm=cfg.clip_norm,
                            grad_scale=grad_scale, exact_norm=True)
         bad = int(norm[1].item())
         if bad:
             raise NonFiniteGradientError(
-                f"non-finite gradient at optimizer step {self.opt.step + 1}: "
+                f"non-finite gradient at optimizer step {self.step_count + 1}: "
                 f"|w|_nan={int(torch.isnan(gw * grad_scale).sum())}, "
                 f"|b|_nan={int(torch.isnan(gb * grad_scale).sum())}")
-        self.opt.step += 1
+        self.step_count += 1
         return W, b
 
     def write_back(self):
+        """Commit moments and step count together, as apply_update mutates them
+        (policy.py:241-246); called after the last minibatch and, when a minibatch
+        raises, for the updates completed before it."""
+        self.opt.step = self.step_count
         self.opt.m_weights = self.m_w.cpu().numpy()
         self.opt.v_weights = self.v_w.cpu().numpy()
         self.opt.m_bias = self.m_b.cpu().numpy()
@@ -500,12 +546,12 @@ def train_step(batch: TrainBatch, params, opt, config: TrainerConfig = TrainerCo
         torch.zeros(0, dtype=torch.float64, device=dev)                 # 296
     batch.advantages = adv.cpu().numpy()
     decoupled = config.objective == "decoupled"
+    eta_mask, behav_cap = _ext(config, "eta_mask"), _ext(config, "behav_weight_cap")
     versions = None
-    if config.eta_mask >= 0:
-        if batch.versions is None:
+    if eta_mask >= 0:
+        if getattr(batch, "versions", None) is None:
             raise BatchError("eta_mask needs per-token versions in the batch")
         versions = _d(batch.versions, torch.int32, dev)
-    adam_cfg = config.adam
     dadam = _DeviceAdam(opt, dev)
 
     items, plan, gather, group_cu, n_groups = plan_step(
@@ -514,37 +560,41 @@ def train_step(batch: TrainBatch, params, opt, config: TrainerConfig = TrainerCo
     loss_sum = clip_sum = ratio_sum = 0.0
     token_total = excluded = micro_count = updates = 0
     stats = torch.zeros(8, dtype=torch.float64, device=dev)
-    for m, traj_ids in enumerate(items):
-        gw = torch.zeros_like(W)
-        gb = torch.zeros_like(b)
-        stats.zero_()
-        base = int(plan.mb_offsets[m]) + m
-        for g in range(int(n_groups[m])):
-            lo, hi = int(group_cu[base + g]), int(group_cu[base + g + 1])
-            rows = gather[lo:hi]
-            Xg = X.index_select(0, rows.long())
-            logits = _linear_logits(Xg, W, b)
-            dl, _ = K.ppo_fwd_bwd(logits, toks, behav, prox, adv, clip_eps=config.clip_eps,
-                                  decoupled=decoupled, versions=versions,
-                                  current_version=params.version, eta_mask=config.eta_mask,
-                                  behav_weight_cap=config.behav_weight_cap, row_index=rows,
-                                  dlogits=logits, stats=stats)
-            gw += dl.t() @ Xg
-            gb += dl.sum(dim=0)
-            micro_count += 1
-        s = stats.cpu().numpy()
-        n_valid = int(s[1])
-        n = max(n_valid, 1)
-        # dl = -(d obj/d logits), so gw = -grad_w_sum and the reference's scale -1/n
-        # becomes +1/n (sign flips are exact)
-        W, b = dadam.step(W, b, gw, gb, adam_cfg, grad_scale=1.0 / n)    # 329-331
-        updates += 1
-        loss_sum += -float(s[0])
-        clip_sum += float(s[2])
-        ratio_sum += float(s[3])
-        excluded += int(s[4])
-        token_total += n_valid
-    dadam.write_back()
+    try:
+        for m, traj_ids in enumerate(items):                             # 309-334
+            gw = torch.zeros_like(W)
+            gb = torch.zeros_like(b)
+            stats.zero_()
+            base = int(plan.mb_offsets[m]) + m
+            for g in range(int(n_groups[m])):
+                lo, hi = int(group_cu[base + g]), int(group_cu[base + g + 1])
+                rows = gather[lo:hi]
+                Xg = X.index_select(0, rows.long())
+                logits = _linear_logits(Xg, W, b)
+                dl, _ = K.ppo_fwd_bwd(logits, toks, behav, prox, adv, clip_eps=config.clip_eps,
+                                      decoupled=decoupled, versions=versions,
+                                      current_version=params.version, eta_mask=eta_mask,
+                                      behav_weight_cap=behav_cap, row_index=rows,
+                                      dlogits=logits, stats=stats)
+                gw += dl.t() @ Xg
+                gb += dl.sum(dim=0)
+                micro_count += 1
+            s = stats.cpu().numpy()
+            n_valid = int(s[1])
+            n = max(n_valid, 1)
+            # dl = -(d obj/d logits), so gw = -grad_w_sum and the reference's scale -1/n
+            # becomes +1/n (sign flips are exact)
+            W, b = dadam.step(W, b, gw, gb, config.adam, grad_scale=1.0 / n)  # 329-331
+            updates += 1
+            loss_sum += -float(s[0])
+            clip_sum += float(s[2])
+            ratio_sum += float(s[3])
+            excluded += int(s[4])
+            token_total += n_valid
+    finally:
+        # a raising minibatch leaves opt with the updates before it, moments and step
+        # together, as the reference's in-place apply_update does
+        dadam.write_back()
     d = max(token_total, 1)
     out_stats = TrainStepStats(step_index=batch.step_index, loss=loss_sum / d,
                                clip_fraction=clip_sum / d, mean_ratio=ratio_sum / d,

@@ -2,12 +2,15 @@
 kernel path (row_warp / row_ring / cluster ring / TMEM), all logits dtypes, both
 objectives, masks, row_index permutations, in-place backward, entropy on/off, and
 injected NaN / +-inf / extreme logits — each case against the float64 oracle
-(trainer.py:150-195 restated).  Integer counters must match exactly."""
+(trainer.py:150-195 restated) at the tolerances of tests/parity.py: lp 1e-5 for every
+dtype, dlogits on 100% of the elements, counters exact except identified clip-boundary
+tokens."""
 import numpy as np
 import pytest
 import torch
 
 import oracle as O
+import parity as PY
 
 pytestmark = pytest.mark.gpu
 
@@ -15,7 +18,6 @@ if torch.cuda.is_available():
     from paper_2505_24298_b200 import kernels as K
 
 DT = {"f32": torch.float32, "bf16": torch.bfloat16, "f16": torch.float16}
-TOL = {"f32": 1e-5, "bf16": 2e-2, "f16": 2e-2}
 VOCABS = [7, 100, 4097, 8192, 32000, 50257, 65536, 128256, 151936, 152064, 200003, 262144,
           151937, 16381, 98305]  # + unaligned TMEM / ring rows and a chunk-boundary case
 
@@ -72,24 +74,24 @@ def test_k1_k2_fuzz(seed):
     K.logprob_fwd(lg, cu(c["tokens"]), row_index=ri, lp_out=lp, entropy_out=ent,
                   with_entropy=c["ent"])
     got_lp = lp.cpu().numpy()
-    fin = np.isfinite(ref_lp)
-    assert np.array_equal(np.isfinite(got_lp), fin) or c["special"] in (1, 2)
-    tol = TOL[dt]
-    assert np.allclose(got_lp[fin], ref_lp[fin], rtol=tol, atol=tol * 10)
+    # K1 computes in fp32 from the exact rounded inputs the oracle sees: 1e-5 for every dtype
+    PY.check_lp(got_lp, ref_lp, what=f"K1 lp seed {seed}")
+    if c["ent"]:
+        with np.errstate(invalid="ignore", over="ignore"):
+            ref_ent = O.token_entropy(c["x64"])
+        fe = np.isfinite(ref_ent) & np.isfinite(ref_lp)  # the oracle's 0 log 0 := 0 also
+        # turns rows with a NaN / +inf logit into H = 0; the kernels give NaN there
+        err = np.abs(ent.cpu().numpy()[fe] - ref_ent[fe])
+        assert np.all(err <= 1e-4 * (1.0 + np.abs(ref_ent[fe]))), float(err.max())
     dl = lg if c["inplace"] else None
     dl, st = K.ppo_fwd_bwd(lg, cu(c["tokens"]), cu(c["behav"]), cu(c["prox"]), cu(c["adv"]),
                            decoupled=c["decoupled"], versions=cu(c["versions"]),
                            current_version=100, eta_mask=c["eta"], row_index=ri, dlogits=dl)
     s = st.cpu().numpy()
-    rs = ref["stats"]
-    assert s[7] == T
-    # validity can differ from the float64 reference only through lp within the bf16/fp32
-    # tolerance at a clip boundary; the counters are exact otherwise
-    assert abs(s[1] - rs[1]) <= 1 and abs(s[4] - rs[4]) <= 1 and s[5] == rs[5]
+    # counters exact; n_clipped may differ only by the identified clip-boundary tokens
+    bnd = PY.boundary_tokens(ref, 0.2)
+    PY.check_counters(s, ref["stats"], int(bnd.sum()), what=f"seed {seed}")
+    # dlogits: 100% of the elements of every row (boundary rows excepted)
     got = dl.double().cpu().numpy()
-    want = ref["dlogits"][perm]
-    rowok = np.isfinite(want).all(axis=1) & (np.abs(ref["coef"][perm]) > 0)
-    if rowok.any():
-        err = np.abs(got[rowok] - want[rowok])
-        bound = tol * np.abs(want[rowok]) + tol * 1e-3 * np.abs(ref["coef"][perm][rowok])[:, None] + 1e-30
-        assert (err <= bound * 10).mean() > 0.999
+    PY.check_dlogits(got, ref["dlogits"][perm], ref["coef"][perm], c["tokens"][perm], dt,
+                     skip_rows=bnd[perm], what=f"K2 dlogits seed {seed} ({dt}, V={c['V']})")
