@@ -1,7 +1,7 @@
 """Benchmark of the decoupled-PPO training hot path on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config cfg2|cfg1|cfg3|cfg5]
+                    [--config cfg1|cfg2|cfg3|cfg4|cfg5] [--scaling weak|strong]
 
 One step = one pass of the hot path over one synthetic global batch of the
 named shape: K3 advantages, K4/K5 allocation + packing of every minibatch, K1
@@ -50,7 +50,7 @@ CONFIGS = {
     # configs[3]: GRPO group-normalised advantages, 16 samples/prompt, versions lag 0..8
     "cfg4": dict(workload="GRPO 16 samples/prompt, mixed versions (BASELINE configs[3])",
                  vocab=151936, rollouts=1024, prompts=64, len_lo=128, len_hi=8192, dtype="bf16",
-                 budget=32768, minibatches=4, eta=8, adv_norm="group"),
+                 budget=32768, minibatches=4, eta=8, adv_norm="group_sequence"),
     # configs[4]: heavy-tailed stress, reference Pareto sampler (timeline.py:84-90)
     "cfg5": dict(workload="stress: 4096 rollouts, Pareto lengths 64-32768 (BASELINE configs[4])",
                  vocab=151936, rollouts=4096, prompts=1024, pareto=(1.2, 64.0, 32768, 64),
@@ -125,6 +125,14 @@ def fused_head_bench(cfg, dev, iters=5):
                 speedup_vs_unfused=base / fused)
 
 
+def lengths_label(cfg) -> str:
+    if "pareto" in cfg:
+        a, sc, cap, fl = cfg["pareto"]
+        return (f"{sc:g} * (1 + Pareto({a:g})) clipped to [1, {cap}], floored at {fl} "
+                f"(timeline.py:84-90), seed 0")
+    return f"U[{cfg['len_lo']},{cfg['len_hi']}] seed 0"
+
+
 def workload_arrays(cfg, n_copies=1, seed=0):
     """Synthetic rollouts: lengths U[lo, hi], tokens uniform, rewards +-5, prompt groups."""
     rng = np.random.default_rng(seed)
@@ -148,48 +156,142 @@ def workload_arrays(cfg, n_copies=1, seed=0):
                 versions=versions, T=T, n=n)
 
 
-# ------------------------------------------------------------------ CPU baseline (oracle)
-def _cpu_worker(job):
-    seed, rows, V = job
+# ------------------------------------------------------------------ CPU reference path
+def _ref_log_softmax():
+    """policy.log_softmax (policy.py:145-147) from the UNMODIFIED reference install in
+    baseline/_ref when present (the reference's own code), else the oracle's restatement
+    of it (identical numpy calls).  Returns (fn, source)."""
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(os.path.join(path, "asyncrl")):
+        if path not in sys.path:
+            sys.path.insert(0, path)
+        try:
+            import asyncrl.policy as P
+            return P.log_softmax, "asyncrl.policy.log_softmax (baseline/_ref)"
+        except Exception:  # pragma: no cover - broken install
+            pass
     import oracle as O
+    return O.log_softmax, "oracle.log_softmax (restatement of policy.py:145-147)"
+
+
+def _ref_tokens(log_softmax, x, tok, behav, adv, clip_eps=0.2):
+    """The reference's per-token work on given logits, one micro-batch (no entropy):
+    trainer.py:128-137 (prox = log_softmax(x)[tok], policy.py:159-163) and then
+    trainer.py:163-195 (log_softmax again under the current params, ratios, clip,
+    objective, coef, the score residual coef * (onehot - softmax) and the counters).
+    The linear model's GEMMs (163's feats @ W.T, 183-184) are the model, out of scope."""
+    ar = np.arange(len(tok))
+    prox = log_softmax(x)[ar, tok]                                       # 134
+    all_lp = log_softmax(x)                                              # 163
+    lp = all_lp[ar, tok]
+    scale = np.exp(prox - behav)
+    ratio = np.exp(lp - prox)
+    valid = np.isfinite(scale) & np.isfinite(ratio)
+    term_plain = ratio * adv
+    term_clip = np.clip(ratio, 1 - clip_eps, 1 + clip_eps) * adv
+    objective = np.where(valid, scale * np.minimum(term_plain, term_clip), 0.0)
+    take_plain = (term_plain <= term_clip) & valid
+    coef = np.where(take_plain, scale * adv * ratio, 0.0)
+    resid = -np.exp(all_lp)                                              # 180-182
+    resid[ar, tok] += 1.0
+    resid *= coef[:, None]
+    return (float(objective.sum()), int(np.count_nonzero(valid)),
+            int(np.count_nonzero(valid & (term_clip < term_plain))),
+            float(np.where(valid, ratio, 0.0).sum()))
+
+
+def _cpu_worker(job):
+    """One process: `rows` tokens of bf16-valued N(0, 2^2) logits, processed in
+    micro-batch chunks of `chunk` rows (memory), timed around the reference work only."""
+    seed, rows, V, chunk = job
+    log_softmax, _ = _ref_log_softmax()
     rng = np.random.default_rng(seed)
     x = rng.standard_normal((rows, V), dtype=np.float32) * 2.0
     x = (x.view(np.uint32) & 0xFFFF0000).view(np.float32).astype(np.float64)  # bf16 values
     tok = rng.integers(0, V, size=rows)
-    t0 = time.perf_counter()
-    lp = O.token_logprobs(x, tok)           # K1: prox log-probs (trainer.py:128-137)
-    O.token_entropy(x)
-    prox = lp + rng.normal(0, 0.02, size=rows)
-    behav = prox + rng.normal(0, 0.1, size=rows)
+    behav = rng.normal(-12.0, 0.3, size=rows)
     adv = rng.normal(size=rows)
-    O.surrogate_terms(x, tok, behav, prox, adv)  # K2: loss + dlogits (trainer.py:150-195)
+    t0 = time.perf_counter()
+    for lo in range(0, rows, chunk):
+        hi = min(rows, lo + chunk)
+        _ref_tokens(log_softmax, x[lo:hi], tok[lo:hi], behav[lo:hi], adv[lo:hi])
     return rows, time.perf_counter() - t0
 
 
-def cpu_baseline(V, target_s=10.0, workers=None):
-    """Oracle K1+K2 math on a bounded sample, one process per host core."""
-    workers = workers or os.cpu_count() or 1
-    r, dt = _cpu_worker((12345, 2, V))
-    per_row = dt / 2
-    mem_rows = max(1, int(24e9 / (V * 8 * 8) / workers))
-    rows = int(max(2, min(512, mem_rows, target_s / max(per_row, 1e-6))))
-    ctx = mp.get_context("fork")
-    t0 = time.perf_counter()
-    with ctx.Pool(workers) as pool:
-        res = pool.map(_cpu_worker, [(1000 + i, rows, V) for i in range(workers)])
-    wall = time.perf_counter() - t0
-    done = sum(x[0] for x in res)
+def _cpu_model() -> str:
     cpu = platform.processor() or ""
     try:
         with open("/proc/cpuinfo") as f:
             cpu = next((l.split(":", 1)[1].strip() for l in f if l.startswith("model name")), cpu)
     except OSError:
         pass
-    return dict(value=done / wall, unit="tokens/s", cores=workers, kind="port",
-                sample=f"{done} tokens ({workers} procs x {rows} rows) of V={V} bf16-valued "
-                       f"logits through the float64 numpy oracle (K1 logprob+entropy, K2 "
-                       f"loss+dlogits); host: {cpu}",
-                wall_s=wall)
+    return cpu
+
+
+def _chunk_rows(V):
+    # micro-batch-sized blocks (~256 MB float64 per array; the reference runs a whole
+    # micro-batch per call, trainer.py:321) within host memory for one process per core
+    return max(1, min(1024, int(256e6 / (V * 8))))
+
+
+def cpu_rate(V, rows_per_proc, procs):
+    """Reference per-token work on `procs` host processes (one per core), each over
+    `rows_per_proc` tokens; returns (tokens/s by wall clock, tokens, wall seconds)."""
+    chunk = _chunk_rows(V)
+    jobs = [(1000 + i, rows_per_proc, V, chunk) for i in range(procs)]
+    if procs == 1:
+        done, wall = _cpu_worker(jobs[0])
+        return done / wall, done, wall
+    ctx = mp.get_context("fork")
+    with ctx.Pool(procs) as pool:
+        pool.map(_cpu_worker, [(7, 1, V, 1)] * procs)  # fork + import warm-up, untimed
+        t0 = time.perf_counter()
+        res = pool.map(_cpu_worker, jobs)
+        wall = time.perf_counter() - t0
+    done = sum(r[0] for r in res)
+    return done / wall, done, wall
+
+
+def cpu_baseline(V, target_s=10.0, workers=None):
+    """The reference's per-token path (``_ref_tokens``) on the host: 1 core and all cores,
+    each on a bounded sample of about target_s seconds."""
+    workers = workers or os.cpu_count() or 1
+    probe_rows = max(2, _chunk_rows(V))
+    r1, _, dt1 = cpu_rate(V, probe_rows, 1)                 # per-core rate probe
+    rows1 = int(max(2, min(4096, r1 * target_s)))
+    v1, n1, _ = cpu_rate(V, rows1, 1)
+    mem_rows = max(1, int(24e9 / (V * 8 * 8) / workers))
+    rowsN = int(max(2, min(4096, mem_rows, v1 * target_s)))
+    vN, nN, wN = cpu_rate(V, rowsN, workers)
+    _, src = _ref_log_softmax()
+    return dict(value=vN, unit="tokens/s", cores=workers, kind="port",
+                cores_1=v1, cores_all=vN, cpu_model=_cpu_model(), os_cpu_count=os.cpu_count(),
+                sample=(f"V={V} bf16-valued logits; 1 core: {n1} tokens; {workers} cores: "
+                        f"{nN} tokens ({workers} procs x {rowsN}); per token the reference's "
+                        f"2 log-softmax passes (prox trainer.py:134, loss 163), ratios, clip, "
+                        f"objective, coef and the score residual (163-195), no entropy; "
+                        f"log_softmax = {src}"),
+                wall_s=wN)
+
+
+def cfg1_full_cpu(workers=None):
+    """BASELINE configs[0] IN FULL on the host: all 70,843 tokens of cfg1 (V = 32,000,
+    seed-0 lengths) through the reference's per-token path, every core."""
+    workers = workers or os.cpu_count() or 1
+    cfg = CONFIGS["cfg1"]
+    T = int(workload_arrays(cfg)["T"])
+    per = [T // workers + (1 if i < T % workers else 0) for i in range(workers)]
+    chunk = _chunk_rows(cfg["vocab"])
+    ctx = mp.get_context("fork")
+    with ctx.Pool(workers) as pool:
+        pool.map(_cpu_worker, [(7, 1, cfg["vocab"], 1)] * workers)
+        t0 = time.perf_counter()
+        res = pool.map(_cpu_worker, [(2000 + i, n, cfg["vocab"], chunk)
+                                     for i, n in enumerate(per) if n])
+        wall = time.perf_counter() - t0
+    done = sum(r[0] for r in res)
+    return dict(tokens=done, wall_s=wall, tokens_per_s=done / wall, cores=workers,
+                note="cfg1 in full (no sampling, no extrapolation)")
 
 
 def run_reference(args, cfg):
@@ -197,22 +299,38 @@ def run_reference(args, cfg):
     if rank != 0:
         return
     V = cfg["vocab"]
-    times, vals = [], []
-    base = None
+    workers = os.cpu_count() or 1
+    # 1-core figure (bounded sample) once; each step is an all-core bounded sample
+    r1, _, _ = cpu_rate(V, max(2, _chunk_rows(V)), 1)
+    rows1 = int(max(2, min(4096, r1 * args.ref_seconds)))
+    v1, n1, _ = cpu_rate(V, rows1, 1)
+    mem_rows = max(1, int(24e9 / (V * 8 * 8) / workers))
+    rowsN = int(max(2, min(4096, mem_rows, v1 * args.ref_seconds)))
+    times, vals, toks = [], [], 0
     for i in range(args.warmup + args.steps):
-        b = cpu_baseline(V, target_s=args.ref_seconds)
+        vN, nN, wN = cpu_rate(V, rowsN, workers)
         if i >= args.warmup:
-            times.append(b["wall_s"])
-            vals.append(b["value"])
-            base = b
+            times.append(wN)
+            vals.append(vN)
+            toks = nN
     value = float(np.mean(vals))
+    _, src = _ref_log_softmax()
+    full = cfg1_full_cpu(workers) if not args.no_cfg1_full else None
     line = dict(metric=METRIC, value=value, unit="tokens/s", n_gpus=args.gpus, steps=args.steps,
                 warmup=args.warmup, ms_per_step=1e3 * float(np.mean(times)),
                 higher_is_better=True, scaling="weak", vs_baseline=None, dtype="f64",
                 data="synthetic", impl="reference",
-                config=dict(workload=cfg["workload"], vocab=V, note="bounded CPU sample per step"),
-                cpu_baseline=dict(value=value, unit="tokens/s", cores=base["cores"],
-                                  kind=base["kind"], sample=base["sample"]),
+                config=dict(workload=cfg["workload"], vocab=V,
+                            note=f"each step: {toks} tokens ({workers} procs x {rowsN}) of the "
+                                 f"config's logits shape, a bounded sample"),
+                cpu_baseline=dict(value=value, unit="tokens/s", cores=workers, kind="port",
+                                  cores_1=v1, cores_all=value, cpu_model=_cpu_model(),
+                                  sample=(f"{toks} tokens per step on {workers} cores, {n1} on "
+                                          f"1 core; per token the reference's 2 log-softmax "
+                                          f"passes (trainer.py:134, 163), ratios, clip, "
+                                          f"objective, coef, score residual (163-195), no "
+                                          f"entropy; log_softmax = {src}")),
+                cfg1_full=full,
                 e2e=dict(value=value, unit="tokens/s", h2d_bytes_per_step=0,
                          d2h_bytes_per_step=0))
     print(json.dumps(line), flush=True)
@@ -283,14 +401,21 @@ def run_ours(args, cfg):
     dev = torch.device("cuda", local_dev)
     if world > 1:
         if args.dist_backend == "nccl":
+            # the communicator's own report (ranks, NVLS/NVLink transport) on stderr
+            if os.environ.get("NCCL_DEBUG", "").upper() not in ("INFO", "TRACE"):
+                os.environ["NCCL_DEBUG"] = "INFO"
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,ENV")
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(args.dist_backend)
     from paper_2505_24298_b200 import kernels as K
-    from paper_2505_24298_b200.hotpath import DecoupledPPOStep, HotPathConfig, PackedRollouts
+    from paper_2505_24298_b200.hotpath import (DecoupledPPOStep, HostRollouts, HotPathConfig,
+                                               PackedRollouts, load_summary)
 
-    # weak scaling: the global batch is N copies of the config's batch shape
-    W = workload_arrays(cfg, n_copies=world)
+    # weak scaling: the global batch is N copies of the config's batch shape; strong:
+    # the config's batch itself, split over the N ranks
+    strong = args.scaling == "strong"
+    W = workload_arrays(cfg, n_copies=1 if strong else world)
     V = cfg["vocab"]
     ldt = torch.bfloat16 if cfg["dtype"] == "bf16" else torch.float32
     C = cfg["budget"]
@@ -328,7 +453,8 @@ def run_ours(args, cfg):
     host = dict(traj_bounds=pin(W["bounds"]), tokens=pin(W["tokens"]),
                 behav=pin(np.zeros(W["T"])), rewards=pin(W["rewards"]),
                 versions=pin(W["versions"]) if "eta" in cfg else None,
-                group_ids=pin(W["group_ids"]) if cfg.get("adv_norm") == "group" else None)
+                group_ids=pin(W["group_ids"]) if cfg.get("adv_norm", "").startswith("group")
+                else None)
     ro = PackedRollouts.from_host(**host, device=dev)
     torch.cuda.synchronize()
 
@@ -388,26 +514,36 @@ def run_ours(args, cfg):
     e2e_steps = max(1, args.e2e_steps)
     res_host = torch.empty((cfg["minibatches"], 8), dtype=torch.float64).pin_memory()
     s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    step(PackedRollouts.from_host(**host, device=dev))  # untimed e2e warm-up
+    # pinned host rollouts: run() uploads the trajectory-level arrays and, per rank, only
+    # the per-token arrays of the trajectories in that rank's micro-batches
+    host_ro = HostRollouts(**host)
+    step(host_ro)  # untimed e2e warm-up
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     s2.record()
     h2d = d2h = 0
     for _ in range(e2e_steps):
-        r = PackedRollouts.from_host(**host, device=dev)
-        h2d = r.h2d_bytes()
-        out = step(r)  # returns host stats (one D2H of the minibatch sums)
+        out = step(host_ro)  # returns host stats (one D2H of the minibatch sums)
+        h2d = runner.h2d_bytes
         d2h = out.minibatch_stats.nbytes
     e2.record()
     torch.cuda.synchronize()
     e2e_ms = s2.elapsed_time(e2) / e2e_steps
     del res_host
 
-    t_max = torch.tensor([ms, e2e_ms, k2_ms, k1_ms], dtype=torch.float64, device=dev)
+    t_max = torch.tensor([ms, e2e_ms, k2_ms, k1_ms, h2d], dtype=torch.float64, device=dev)
+    job_bytes = torch.tensor([float(k1_bytes + k2_bytes)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+        dist.all_reduce(job_bytes)
     ms, e2e_ms = float(t_max[0]), float(t_max[1])
+    h2d_max = int(t_max[4])
+    job_bytes = float(job_bytes[0]) / args.steps  # algorithmic K1 + K2 bytes, all ranks
+    comm = None
+    if world > 1:
+        comm = dict(backend=dist.get_backend(), world_size=dist.get_world_size(),
+                    nccl_debug=os.environ.get("NCCL_DEBUG"))
     T = W["T"]
     if rank == 0:
         peak, peak_src = _peaks()
@@ -430,10 +566,10 @@ def run_ours(args, cfg):
         line = dict(
             metric=METRIC, value=T / (ms * 1e-3), unit="tokens/s", n_gpus=world,
             steps=args.steps, warmup=args.warmup, ms_per_step=ms, higher_is_better=True,
-            scaling="weak", vs_baseline=None, dtype=cfg["dtype"],
+            scaling=args.scaling, vs_baseline=None, dtype=cfg["dtype"],
             data="synthetic (random bf16 logits in rotating HBM buffers; rollouts seeded)",
             config=dict(workload=cfg["workload"], vocab=V, rollouts=W["n"], tokens=T,
-                        lengths=f"U[{cfg['len_lo']},{cfg['len_hi']}] seed 0",
+                        lengths=lengths_label(cfg),
                         micro_token_budget=C, minibatches=cfg["minibatches"],
                         micro_min_groups=hp.micro_min_groups, logits_dtype=cfg["dtype"],
                         l2="inputs > L2: %d rotating %.1f GB logits buffers" % (
@@ -456,8 +592,22 @@ def run_ours(args, cfg):
                             "small device->host read of the plan that sizes the model calls"),
             e2e=dict(value=T / (e2e_ms * 1e-3), unit="tokens/s", h2d_bytes_per_step=h2d,
                      d2h_bytes_per_step=d2h,
-                     note="public API DecoupledPPOStep.run from pinned host rollouts; "
-                          "logits are device-resident model outputs"),
+                     note="public API DecoupledPPOStep.run(HostRollouts) from pinned host "
+                          "rollouts (per-token arrays uploaded only for this rank's "
+                          "micro-batches; bytes of rank 0); logits are device-resident "
+                          "model outputs"),
+            step_roofline=dict(
+                bound="hbm", bytes_per_step=job_bytes, unit="GB/s",
+                achieved=job_bytes / (ms * 1e-3) / 1e9 / world, peak=peak,
+                frac=job_bytes / (ms * 1e-3) / 1e9 / world / peak,
+                note="whole step (K1 + K2 algorithmic bytes; K3/K4/K5 and the host work "
+                     "between launches count as time) per GPU against the copy peak"),
+            data_parallel=dict(world_size=world, scaling=args.scaling, comm=comm,
+                               **load_summary(runner.last_plan.load if runner.last_plan
+                                              else None),
+                               h2d_bytes_per_step_max_rank=h2d_max,
+                               note="micro-batches dealt longest-first by tokens; "
+                                    "efficiency_bound = sum_m mean / sum_m max rank load"),
             gpu_launches=launches,
             gpu_launches_per_step=launches // args.steps,
             clocks=clk.summary(),
@@ -478,12 +628,19 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--config", default=None, choices=sorted(CONFIGS),
+                    help="default: cfg2 (BASELINE configs[1]) for weak scaling, cfg3 "
+                         "(configs[2], the 1/2/4/8-GPU batch) for strong scaling")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: the global batch is N copies of the config's batch; strong: "
+                         "the config's batch split over the N ranks")
+    ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--logit-buffers", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-seconds", type=float, default=6.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cfg1-full", action="store_true",
+                    help="reference arm: skip the full cfg1 run on all host cores")
     ap.add_argument("--no-fused-head", action="store_true",
                     help="skip the auxiliary K7 fused LM-head measurement")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
@@ -492,6 +649,8 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+    if args.config is None:
+        args.config = "cfg3" if args.scaling == "strong" else "cfg2"
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, cfg)

@@ -119,6 +119,69 @@ class PackedRollouts:
                               up(values, torch.float64))
 
 
+    @staticmethod
+    def from_host_meta(host: "HostRollouts", device=None):
+        """The trajectory-level arrays (cu_seqlens, rewards, group ids; GAE values whole,
+        K3 scans every trajectory) uploaded; the per-token arrays allocated on the device
+        and left for ``upload_token_ranges`` (a rank fills only the tokens it trains on)."""
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None else device
+        up = lambda t, dt: None if t is None else t.to(dt).to(dev, non_blocking=True)
+        T = int(host.traj_bounds[-1]) if host.traj_bounds.numel() else 0
+        emp = lambda t, dt: None if t is None else torch.empty(T, dtype=dt, device=dev)
+        return PackedRollouts(up(host.traj_bounds, torch.int64),
+                              host.traj_bounds.numpy().astype(np.int64),
+                              emp(host.tokens, torch.int64), emp(host.behav, torch.float64),
+                              up(host.rewards, torch.float64), emp(host.versions, torch.int32),
+                              up(host.group_ids, torch.int32), up(host.values, torch.float64))
+
+    def upload_token_ranges(self, host: "HostRollouts", ranges) -> int:
+        """Async H2D of the per-token arrays for global token ranges [(lo, hi)] only, at the
+        same offsets (the device arrays stay indexed by global token).  Returns bytes."""
+        n = 0
+        for name in ("tokens", "behav", "versions"):
+            src, dst = getattr(host, name), getattr(self, name)
+            if src is None or dst is None:
+                continue
+            for lo, hi in ranges:
+                dst[lo:hi].copy_(src[lo:hi], non_blocking=True)
+                n += (hi - lo) * dst.element_size()
+        return n
+
+
+@dataclass
+class HostRollouts:
+    """One global batch in formation order on the host (pinned tensors; the output of the
+    native packer, ``pack_trajectories(..., device=None)``).  ``DecoupledPPOStep.run``
+    uploads the trajectory-level arrays whole and the per-token arrays only for the
+    trajectories of this rank's micro-batches (all of them on one GPU)."""
+    traj_bounds: torch.Tensor
+    tokens: torch.Tensor
+    behav: torch.Tensor
+    rewards: torch.Tensor
+    versions: torch.Tensor | None = None
+    group_ids: torch.Tensor | None = None
+    values: torch.Tensor | None = None
+
+    @staticmethod
+    def from_arrays(traj_bounds, tokens, behav, rewards, versions=None, group_ids=None,
+                    values=None, pin: bool = True):
+        def h(x, dt):
+            if x is None:
+                return None
+            t = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x))
+            t = t.to(dt).contiguous()
+            return t.pin_memory() if pin and not t.is_pinned() else t
+        return HostRollouts(h(traj_bounds, torch.int64), h(tokens, torch.int64),
+                            h(behav, torch.float64), h(rewards, torch.float64),
+                            h(versions, torch.int32), h(group_ids, torch.int32),
+                            h(values, torch.float64))
+
+    def h2d_bytes(self) -> int:
+        ts = [self.traj_bounds, self.tokens, self.behav, self.rewards, self.versions,
+              self.group_ids, self.values]
+        return int(sum(t.numel() * t.element_size() for t in ts if t is not None))
+
+
 def _packer():
     try:
         from . import _packer as P  # built by paper_2505_24298_b200.build (gcc)
@@ -128,7 +191,8 @@ def _packer():
     return P
 
 
-def pack_trajectories(trajectories, device=None, pin: bool = True, with_groups: bool = True):
+def pack_trajectories(trajectories, device=None, pin: bool = True, with_groups: bool = True,
+                      upload: bool = True):
     """Replay-buffer trajectories (formation order) -> PackedRollouts on the GPU.
 
     build_train_batch (trainer.py:83-111) without the per-token Python loop: the
@@ -138,7 +202,9 @@ def pack_trajectories(trajectories, device=None, pin: bool = True, with_groups: 
     the dense ids of ``traj.prompt.id`` in first-appearance order (tasks.py:80, the
     harness's n_prompts x n_responses batch, harness.py:93-95).  Returns
     (PackedRollouts, host tensors) — keep the host tensors alive until the copies
-    have completed (e.g. reuse them for the next batch).
+    have completed (e.g. reuse them for the next batch).  ``upload=False`` returns
+    (HostRollouts, host tensors) instead: ``DecoupledPPOStep.run`` then uploads only the
+    tokens of this rank's micro-batches.
     """
     P = _packer()
     trajs = list(trajectories)
@@ -159,6 +225,8 @@ def pack_trajectories(trajectories, device=None, pin: bool = True, with_groups: 
         host["group_ids"] = torch.tensor(g, dtype=torch.int32)
         if pin:
             host["group_ids"] = host["group_ids"].pin_memory()
+    if not upload:
+        return HostRollouts(**host), host
     ro = PackedRollouts.from_host(**host, device=device)
     return ro, host
 
@@ -173,6 +241,8 @@ class StepPlan:
     n_groups: np.ndarray        # host, per minibatch
     micro: list = field(default_factory=list)     # [(m, g, lo, hi)] all micro-batches
     mine: list = field(default_factory=list)      # per minibatch: this rank's [(g, lo, hi)]
+    load: np.ndarray | None = None                # [M, world] tokens dealt to each rank
+    host_seq: tuple | None = None                 # (group_seq_cu, packed_traj) host copies
 
     @property
     def n_micro(self) -> int:
@@ -192,14 +262,17 @@ def lpt_assign(sizes, world_size: int):
     return owner
 
 
-def shard_micro_batches(group_cu, n_groups, mb_offsets, world_size: int, rank: int):
+def shard_micro_batches(group_cu, n_groups, mb_offsets, world_size: int, rank: int,
+                        with_load: bool = False):
     """Host-side DP sharding of a replicated plan.
 
     group_cu / n_groups / mb_offsets use the layout of areal_plan_microbatches.
     Returns (all micro-batches [(m, g, lo, hi)], this rank's [(g, lo, hi)] per
-    minibatch), micro-batches dealt LPT by token count within each minibatch.
+    minibatch), micro-batches dealt LPT by token count within each minibatch; with
+    ``with_load`` also the [M, world] token load of every rank (identical on all ranks).
     """
     micro, mine = [], []
+    load = np.zeros((len(n_groups), world_size), dtype=np.int64)
     for m in range(len(n_groups)):
         base = int(mb_offsets[m]) + m
         groups = [(g, int(group_cu[base + g]), int(group_cu[base + g + 1]))
@@ -207,7 +280,23 @@ def shard_micro_batches(group_cu, n_groups, mb_offsets, world_size: int, rank: i
         micro.extend((m, g, lo, hi) for g, lo, hi in groups)
         owner = lpt_assign([hi - lo for _, lo, hi in groups], world_size)
         mine.append([grp for grp, r in zip(groups, owner) if r == rank])
-    return micro, mine
+        for (g, lo, hi), r in zip(groups, owner):
+            load[m, r] += hi - lo
+    return (micro, mine, load) if with_load else (micro, mine)
+
+
+def load_summary(load: np.ndarray) -> dict:
+    """Data-parallel balance of a plan: the step waits, minibatch by minibatch, for the
+    busiest rank (the statistics all-reduce), so sum_m mean / sum_m max bounds the
+    scaling efficiency the dealing allows."""
+    if load is None or load.size == 0:
+        return dict(rank_tokens=[], max_over_mean=1.0, efficiency_bound=1.0)
+    per_rank = load.sum(axis=0)
+    mx = load.max(axis=1).sum()
+    return dict(rank_tokens=[int(x) for x in per_rank],
+                max_over_mean=float(per_rank.max() / max(per_rank.mean(), 1e-9)),
+                per_minibatch_max_over_mean=[float(r.max() / max(r.mean(), 1e-9)) for r in load],
+                efficiency_bound=float(load.mean(axis=1).sum() / max(mx, 1)))
 
 
 @dataclass
@@ -248,6 +337,8 @@ class DecoupledPPOStep:
         self.k7_flops = 0
         self.record_events = False
         self._readback = None  # pinned buffer for the plan's host read
+        self.h2d_bytes = 0     # host->device bytes of the last run() from HostRollouts
+        self.last_plan = None
 
     # ---- K3
     def advantages(self, ro: PackedRollouts) -> torch.Tensor:
@@ -263,7 +354,7 @@ class DecoupledPPOStep:
     def plan(self, ro: PackedRollouts) -> StepPlan:
         return self._plan_finish(self._plan_launch(ro))
 
-    def _plan_launch(self, ro: PackedRollouts):
+    def _plan_launch(self, ro: PackedRollouts, with_seq: bool = False):
         """Host split + K4, an async read of the plan's sizes into pinned memory, then
         K5: the host later waits for K4 and that read only (K5 and whatever the caller
         queues next, e.g. K3, run while it deals the micro-batches)."""
@@ -282,8 +373,10 @@ class DecoupledPPOStep:
         dplan = K.plan_microbatches(ro.traj_bounds, flat, mb_offsets, mb_token_start,
                                     _device_capacity(cap, [max(mb_tokens)]), c.micro_min_groups)
         # the single host read of the plan: micro-batch sizes drive the model's shapes
+        # (+ which trajectories each micro-batch packs, when the rank uploads only its own)
         M, n_gc = len(items), dplan.group_cu.numel()
-        need = 16 * M + 8 * n_gc
+        n_it = dplan.packed_traj.numel()
+        need = 16 * M + 8 * n_gc + (4 * (n_gc + n_it) + 16 if with_seq else 0)
         if self._readback is None or self._readback.numel() < need:
             self._readback = torch.empty(max(2 * need, 4096), dtype=torch.uint8).pin_memory()
         rb = self._readback
@@ -293,17 +386,25 @@ class DecoupledPPOStep:
         gcu.copy_(dplan.group_cu, non_blocking=True)
         st.copy_(dplan.status[:M], non_blocking=True)
         ng.copy_(dplan.n_groups[:M], non_blocking=True)
+        seq = None
+        if with_seq:
+            o = 8 * n_gc + 16 * M
+            gsc = rb[o:o + 4 * n_gc].view(torch.int32)
+            ptr = rb[o + 4 * n_gc:o + 4 * (n_gc + n_it)].view(torch.int32)
+            gsc.copy_(dplan.group_seq_cu, non_blocking=True)
+            ptr.copy_(dplan.packed_traj, non_blocking=True)
+            seq = (gsc, ptr)
         ready = torch.cuda.Event()
         ready.record()
         gather, _ = K.fill_gather(ro.traj_bounds, dplan, int(sum(mb_tokens)))
         self.launches += 2
-        return items, (dplan, gather, mb_offsets, lens, gcu, st, ng, ready)
+        return items, (dplan, gather, mb_offsets, lens, gcu, st, ng, ready, seq)
 
     def _plan_finish(self, pending) -> StepPlan:
         items, rest = pending
         if rest is None:
             return StepPlan(items, None, None, None, None)
-        dplan, gather, mb_offsets, lens, gcu, st, ng, ready = rest
+        dplan, gather, mb_offsets, lens, gcu, st, ng, ready, seq = rest
         ready.synchronize()
         status, n_groups, group_cu = st.numpy().copy(), ng.numpy().astype(np.int64), \
             gcu.numpy().copy()
@@ -313,9 +414,33 @@ class DecoupledPPOStep:
             raise _status_error(int(status[m]), [int(lens[k]) for k in items[m]],
                                 self.cfg.micro_token_budget)
         sp = StepPlan(items, dplan, gather, group_cu, n_groups)
-        sp.micro, sp.mine = shard_micro_batches(group_cu, n_groups, mb_offsets, self.world,
-                                                self.rank)
+        sp.micro, sp.mine, sp.load = shard_micro_batches(group_cu, n_groups, mb_offsets,
+                                                         self.world, self.rank, with_load=True)
+        if seq is not None:
+            sp.host_seq = (seq[0].numpy().copy(), seq[1].numpy().copy())
+        self.last_plan = sp
         return sp
+
+    def own_token_ranges(self, ro: PackedRollouts, sp: StepPlan):
+        """Global token ranges of the trajectories in this rank's micro-batches, sorted and
+        coalesced (consecutive trajectories merge into one copy)."""
+        gsc, ptraj = sp.host_seq
+        mb_off = sp.device_plan.mb_offsets
+        trajs = []
+        for m, groups in enumerate(sp.mine):
+            base = int(mb_off[m]) + m
+            for g, _, _ in groups:
+                trajs.extend(ptraj[gsc[base + g]:gsc[base + g + 1]].tolist())
+        trajs.sort()
+        b = ro.traj_bounds_host
+        ranges = []
+        for k in trajs:
+            lo, hi = int(b[k]), int(b[k + 1])
+            if ranges and ranges[-1][1] == lo:
+                ranges[-1] = (ranges[-1][0], hi)
+            elif hi > lo:
+                ranges.append((lo, hi))
+        return ranges
 
     def _timed(self, events, fn):
         if not self.record_events:
@@ -354,14 +479,26 @@ class DecoupledPPOStep:
         return prox
 
     # ---- full step
-    def run(self, ro: PackedRollouts, logits_fn, backward_fn=None, update_fn=None,
+    def run(self, ro, logits_fn, backward_fn=None, update_fn=None,
             current_version: int = 0, dlogits_fn=None, prox_head_fn=None) -> StepResult:
+        """``ro`` is a device-resident PackedRollouts, or a HostRollouts (pinned host
+        arrays): then the trajectory-level arrays are uploaded whole and the per-token
+        arrays only for the trajectories this rank trains on (``self.h2d_bytes``)."""
         c = self.cfg
+        host = None
+        if isinstance(ro, HostRollouts):
+            host = ro
+            ro = PackedRollouts.from_host_meta(host, self.device)
+            self.h2d_bytes = sum(t.numel() * t.element_size() for t in (
+                host.traj_bounds, host.rewards, host.group_ids, host.values) if t is not None)
         # K4 first: the plan's one host read waits for K4 only; K5 and K3 run
         # behind it while the host deals the micro-batches and launches the prox pass
-        pending = self._timed(self.k45_events, lambda: self._plan_launch(ro))  # 300-315
+        pending = self._timed(self.k45_events,
+                              lambda: self._plan_launch(ro, with_seq=host is not None))  # 300-315
         adv = self._timed(self.k3_events, lambda: self.advantages(ro))  # trainer.py:296
         sp = self._plan_finish(pending)
+        if host is not None and sp.device_plan is not None:
+            self.h2d_bytes += ro.upload_token_ranges(host, self.own_token_ranges(ro, sp))
         decoupled = c.objective == "decoupled"
         M = len(sp.items)
         fuse0 = c.fuse_first_prox and decoupled and M > 0

@@ -196,7 +196,9 @@ def _device() -> torch.device:
 
 
 def _d(x, dtype, dev):
-    return torch.as_tensor(np.ascontiguousarray(x), dtype=dtype).to(dev)
+    # the reference's parameter snapshots are read-only arrays (policy.py:99-100): a
+    # writable host copy keeps torch from aliasing them
+    return torch.as_tensor(np.require(x, requirements=("C", "W")), dtype=dtype).to(dev)
 
 
 def _rewards(batch) -> np.ndarray:

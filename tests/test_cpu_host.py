@@ -185,3 +185,51 @@ def test_data_parallel_stats_allreduce_gloo_world2():
         assert mine0 + mine1 == ng and mine0 >= 1 and mine1 >= 1  # k_min = world: both busy
         assert np.allclose(a, full, rtol=1e-12, atol=1e-12)
         assert a[1] == full[1] and a[7] == full[7]
+
+
+def test_rank_upload_ranges_cover_exactly_the_rank_tokens():
+    """DP e2e uploads only the per-token arrays of the trajectories in a rank's
+    micro-batches (hotpath.own_token_ranges): over all ranks the ranges tile the
+    non-empty trajectories exactly once, and each rank's ranges hold exactly the tokens
+    its micro-batches pack.  The [M, world] load is identical on every rank."""
+    from types import SimpleNamespace
+    from paper_2505_24298_b200.hotpath import (DecoupledPPOStep, load_summary,
+                                               shard_micro_batches)
+    rng = np.random.default_rng(5)
+    lengths = rng.integers(0, 90, size=60)
+    bounds = np.concatenate([[0], np.cumsum(lengths)]).astype(np.int64)
+    for world in (1, 2, 3, 8):
+        plan, group_cu, n_groups, mb_offsets, packed = _oracle_plan_layout(bounds, 3, 200, world)
+        # group_seq_cu / packed_traj in the C-ABI layout
+        gsc = np.zeros_like(group_cu, dtype=np.int32)
+        ptraj, s = [], 0
+        for m, mb in enumerate(plan):
+            base = int(mb_offsets[m]) + m
+            for g, grp in enumerate(mb["groups"]):
+                gsc[base + g] = s
+                ptraj.extend(mb["traj_ids"][j] for j in grp)
+                s += len(grp)
+            gsc[base + len(mb["groups"])] = s
+        seen = np.zeros(int(bounds[-1]), dtype=np.int64)
+        loads = []
+        for rank in range(world):
+            micro, mine, load = shard_micro_batches(group_cu, n_groups, mb_offsets, world, rank,
+                                                    with_load=True)
+            loads.append(load)
+            sp = SimpleNamespace(mine=mine, host_seq=(gsc, np.array(ptraj, dtype=np.int32)),
+                                 device_plan=SimpleNamespace(mb_offsets=mb_offsets))
+            ro = SimpleNamespace(traj_bounds_host=bounds)
+            ranges = DecoupledPPOStep.own_token_ranges(None, ro, sp)
+            assert all(a[1] < b[0]  # sorted, disjoint and coalesced
+                       for a, b in zip(ranges, ranges[1:]))
+            mine_tokens = np.sort(np.concatenate([packed[lo:hi] for grp in mine
+                                                  for _, lo, hi in grp] or [np.zeros(0, int)]))
+            got = np.concatenate([np.arange(lo, hi) for lo, hi in ranges] or [np.zeros(0, int)])
+            assert np.array_equal(np.sort(got), mine_tokens)
+            seen[got] += 1
+            assert int(load[:, rank].sum()) == len(mine_tokens)
+        assert np.all(seen == 1)
+        assert all(np.array_equal(loads[0], x) for x in loads)
+        summ = load_summary(loads[0])
+        assert sum(summ["rank_tokens"]) == int(bounds[-1])
+        assert 0 < summ["efficiency_bound"] <= 1.0 and summ["max_over_mean"] >= 1.0

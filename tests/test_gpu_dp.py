@@ -51,9 +51,16 @@ def _run(world, rank, port=None, q=None):
             pc = prox.cpu()
             dist.all_reduce(pc)
             prox = pc.cuda()
-        res = runner.run(ro, lambda ph, m, g_, rows: table.index_select(0, rows.long()),
-                         current_version=100)
-        out = (res.minibatch_stats, prox.cpu().numpy(), [len(x) for x in sp.mine], res.microbatches)
+        lf = lambda ph, m, g_, rows: table.index_select(0, rows.long())
+        res = runner.run(ro, lf, current_version=100)
+        # the e2e form: pinned host rollouts, per-token arrays uploaded only for the
+        # trajectories of this rank's micro-batches (strong scaling: the batch is split)
+        from paper_2505_24298_b200.hotpath import HostRollouts
+        host = HostRollouts.from_arrays(bounds, tokens, behav, rewards, versions=versions)
+        res_h = runner.run(host, lf, current_version=100)
+        meta = 8 * (len(bounds) + len(rewards))
+        out = (res.minibatch_stats, prox.cpu().numpy(), [len(x) for x in sp.mine], res.microbatches,
+               res_h.minibatch_stats, runner.h2d_bytes - meta, T)
         if q is not None:
             q.put((rank, out))
         return out
@@ -76,9 +83,14 @@ def test_two_ranks_match_single_rank():
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
-    st0, prox0, mine0, micro0 = res[0]
-    st1, prox1, mine1, _ = res[1]
-    st, prox, _, micro = single
+    st0, prox0, mine0, micro0, sth0, tok_bytes0, T = res[0]
+    st1, prox1, mine1, _, sth1, tok_bytes1, _ = res[1]
+    st, prox, _, micro, sth, tok_bytes, _ = single
+    # host-rollout runs reproduce the device-resident runs bitwise; per-token uploads
+    # partition the batch between the ranks (8 + 8 + 4 bytes per token)
+    assert np.array_equal(sth0, st0) and np.array_equal(sth1, st1) and np.array_equal(sth, st)
+    assert tok_bytes == 20 * T and tok_bytes0 + tok_bytes1 == 20 * T
+    assert 0 < tok_bytes0 < 20 * T and 0 < tok_bytes1 < 20 * T
     assert np.array_equal(st0, st1)                 # every rank holds the same all-reduced sums
     assert np.array_equal(prox0, prox)              # each token's prox comes from one rank, bitwise
     assert micro0 == micro                          # same replicated plan
