@@ -122,6 +122,29 @@ const char* areal_status_string(int status);
 /* Number of stats slots a K2 launch uses in the workspace (diagnostics). */
 size_t areal_workspace_bytes(void);
 
+/* ---- kernel-selection tuning (debug / A-B API) ----------------------------
+ * The shipped kernel choice is a fixed function of shapes, dtypes and
+ * alignment.  These knobs override it for A/B measurement and for tests of the
+ * non-default variants; nothing is read from the environment.  Values are
+ * validated (AREAL_ERR_INVALID_ARGUMENT otherwise); AREAL_TUNE_DEFAULT (-1)
+ * restores the shipped rule.  Process-global, read at each launch: set them
+ * before launching, not concurrently with launches on other threads. */
+typedef enum {
+  AREAL_TUNE_K2_CLUSTER_SIZE = 0,    /* {2,4,8}: force a >= vocab split of the ring K2  */
+  AREAL_TUNE_K2_TMEM = 1,            /* 0: ring/cluster K2 instead of the TMEM kernel   */
+  AREAL_TUNE_K2_TMEM_STREAM = 2,     /* 0: rows beyond TMEM+ring do not stream chunks   */
+  AREAL_TUNE_K2_TMEM_UNALIGNED = 3,  /* 0: unaligned rows on the row-CTA kernel         */
+  AREAL_TUNE_K1_RING_UNALIGNED = 4,  /* 0: unaligned K1 rows on the row-CTA kernel      */
+  AREAL_TUNE_K2_SMALL_ROWCTA_KB = 5, /* [0, 1024]: short-row kernel up to this row size */
+  AREAL_TUNE_ROWCTA = 6,             /* 0: unaligned rows on the one-warp kernel        */
+  AREAL_TUNE_K7_NT = 7,              /* {4,8}: K7 N-tiles per unit                      */
+  AREAL_TUNE_K7_GROUP = 8,           /* [1,16]: K7 vocab blocks per token tile          */
+  AREAL_TUNE_COUNT = 9
+} areal_tune_t;
+#define AREAL_TUNE_DEFAULT (-1)
+int areal_set_tuning(int knob, int64_t value);
+int areal_get_tuning(int knob, int64_t* value);
+
 /* ---- K1: log-softmax-gather (+ entropy) ----------------------------------
  * Replaces recompute_prox_logprobs (trainer.py:128-137) ->
  * batch_token_log_probs (policy.py:159-163) -> log_softmax (policy.py:145-147)

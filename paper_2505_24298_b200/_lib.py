@@ -13,8 +13,6 @@ import torch  # noqa: F401  (load torch's CUDA runtime before the library)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libareal_b200.so")
-# tuning builds (tools/variants.py) can be selected explicitly; default: the in-tree build
-LIB_PATH = os.environ.get("AREAL_B200_LIB") or LIB_PATH
 
 ABI_VERSION = 1
 N_STATS = 8
@@ -72,10 +70,18 @@ class AdamParams(ctypes.Structure):
 
 ADAM_MAX_TENSORS = 32
 
+# areal_tune_t (kernel-selection overrides; -1 = the shipped rule)
+TUNE_KNOBS = {"k2_cluster_size": 0, "k2_tmem": 1, "k2_tmem_stream": 2, "k2_tmem_unaligned": 3,
+              "k1_ring_unaligned": 4, "k2_small_rowcta_kb": 5, "rowcta": 6, "k7_nt": 7,
+              "k7_group": 8}
+TUNE_DEFAULT = -1
+
 _SIGS = {
     "areal_abi_version": ([], c_i32),
     "areal_status_string": ([ctypes.c_int], ctypes.c_char_p),
     "areal_workspace_bytes": ([], c_sz),
+    "areal_set_tuning": ([ctypes.c_int, c_i64], ctypes.c_int),
+    "areal_get_tuning": ([ctypes.c_int, ctypes.POINTER(c_i64)], ctypes.c_int),
     "areal_logprob_fwd": ([c_vp, c_i64, ctypes.c_int, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp,
                            ctypes.c_int, c_vp, c_sz, c_vp], ctypes.c_int),
     "areal_ppo_fwd_bwd": ([c_vp, c_i64, c_vp, c_i64, ctypes.c_int, c_i64, c_i64, c_vp, c_vp,
@@ -105,6 +111,15 @@ class ArealError(RuntimeError):
     def __init__(self, status: int, where: str):
         self.status = status
         super().__init__(f"{where}: {status_string(status)} (status {status})")
+
+
+def use_library(path: str) -> None:
+    """Select a non-default build (tools/variants.py tuning builds) before the first
+    load(); the product path always loads the in-tree libareal_b200.so."""
+    global LIB_PATH
+    if _LIB is not None:
+        raise RuntimeError("library already loaded from " + LIB_PATH)
+    LIB_PATH = os.path.abspath(path)
 
 
 def load() -> ctypes.CDLL:

@@ -1,4 +1,6 @@
 // capi.cu — library-level entry points of libareal_b200.so.
+#include <atomic>
+
 #include "common.cuh"
 
 extern "C" int areal_abi_version(void) { return AREAL_ABI_VERSION; }
@@ -21,4 +23,39 @@ extern "C" const char* areal_status_string(int status) {
     case AREAL_ERR_BAD_CLIP_EPS: return "clip_eps must be in (0, 1)";
     default: return "unknown status";
   }
+}
+
+// ---- kernel-selection overrides (areal_tune_t); -1 everywhere = the shipped rules
+static std::atomic<int64_t> g_tuning[AREAL_TUNE_COUNT] = {-1, -1, -1, -1, -1, -1, -1, -1, -1};
+
+int64_t areal::tuning(int knob) {
+  return (knob >= 0 && knob < AREAL_TUNE_COUNT) ? g_tuning[knob].load(std::memory_order_relaxed) : -1;
+}
+
+static bool tuning_valid(int knob, int64_t v) {
+  if (v == AREAL_TUNE_DEFAULT) return true;
+  switch (knob) {
+    case AREAL_TUNE_K2_CLUSTER_SIZE: return v == 2 || v == 4 || v == 8;
+    case AREAL_TUNE_K2_TMEM:
+    case AREAL_TUNE_K2_TMEM_STREAM:
+    case AREAL_TUNE_K2_TMEM_UNALIGNED:
+    case AREAL_TUNE_K1_RING_UNALIGNED:
+    case AREAL_TUNE_ROWCTA: return v == 0 || v == 1;
+    case AREAL_TUNE_K2_SMALL_ROWCTA_KB: return v >= 0 && v <= 1024;
+    case AREAL_TUNE_K7_NT: return v == 4 || v == 8;
+    case AREAL_TUNE_K7_GROUP: return v >= 1 && v <= 16;
+    default: return false;
+  }
+}
+
+extern "C" int areal_set_tuning(int knob, int64_t value) {
+  if (knob < 0 || knob >= AREAL_TUNE_COUNT || !tuning_valid(knob, value)) return AREAL_ERR_INVALID_ARGUMENT;
+  g_tuning[knob].store(value, std::memory_order_relaxed);
+  return AREAL_OK;
+}
+
+extern "C" int areal_get_tuning(int knob, int64_t* value) {
+  if (knob < 0 || knob >= AREAL_TUNE_COUNT || value == nullptr) return AREAL_ERR_INVALID_ARGUMENT;
+  *value = g_tuning[knob].load(std::memory_order_relaxed);
+  return AREAL_OK;
 }

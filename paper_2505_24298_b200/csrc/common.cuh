@@ -362,3 +362,9 @@ __device__ __forceinline__ float2 exp2_poly3(float2 x_in) {
   return make_float2(x_in.x == x_in.x ? rx : x_in.x, x_in.y == x_in.y ? ry : x_in.y);
 }
 }  // namespace areal
+
+namespace areal {
+// ------------------------------------------------------------------ host-side tuning table
+// areal_set_tuning / areal_get_tuning (capi.cu); AREAL_TUNE_DEFAULT = shipped rule.
+int64_t tuning(int knob);
+}  // namespace areal

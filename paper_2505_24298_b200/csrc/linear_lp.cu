@@ -561,7 +561,7 @@ extern "C" int areal_linear_logprob_fwd(const void* hidden, int64_t ld_hidden, c
   {
     // group: minimise the L2 working set of the units in flight, (in_flight / group)
     // H tiles + group W blocks of nt * 256 columns (see unit_xy).  nt = 8 N-tiles per
-    // unit; 4 (smaller W blocks, AREAL_K7_NT=4) measured no faster at d = 1536 / 3584
+    // unit; 4 (smaller W blocks, AREAL_TUNE_K7_NT) measured no faster at d = 1536 / 3584
     // (profiles/r01_k7_nt_group_sweep.txt)
     const double in_flight = cg == 2 ? sms / 2 : sms;
     int best_g = 1, best_nt = kMaxNT;
@@ -570,10 +570,8 @@ extern "C" int areal_linear_logprob_fwd(const void* hidden, int64_t ld_hidden, c
       const double bytes = (in_flight / gsz) * tm * (double)dim * 2 + gsz * (double)best_nt * BN * dim * 2;
       if (bytes < best_bytes - 1.0) best_g = gsz, best_bytes = bytes;
     }
-    const char* env_nt = getenv("AREAL_K7_NT");
-    if (env_nt && (atoi(env_nt) == 4 || atoi(env_nt) == 8)) best_nt = atoi(env_nt);
-    const char* env = getenv("AREAL_K7_GROUP");
-    if (env && atoi(env) >= 1) best_g = atoi(env);
+    if (tuning(AREAL_TUNE_K7_NT) > 0) best_nt = (int)tuning(AREAL_TUNE_K7_NT);
+    if (tuning(AREAL_TUNE_K7_GROUP) > 0) best_g = (int)tuning(AREAL_TUNE_K7_GROUP);
     a.nt = best_nt;
     a.vb = best_nt * BN;
     a.n_vb = (int32_t)((vocab + a.vb - 1) / a.vb);

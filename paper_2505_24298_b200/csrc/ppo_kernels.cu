@@ -723,27 +723,17 @@ static int launch_ring(PpoArgs a, cudaStream_t stream, int cs_force) {
     if (CS < 0) return AREAL_ERR_UNSUPPORTED;
     if (cs_force > 0) CS = cs_force;
     {
-      // tuning knob: AREAL_CLUSTER_SIZE in {2, 4, 8} forces a larger vocab split
-      static const int env_cs = [] {
-        const char* s = getenv("AREAL_CLUSTER_SIZE");
-        const int v = s ? atoi(s) : 0;
-        return (v == 2 || v == 4 || v == 8) ? v : 0;
-      }();
-      if (env_cs > CS) CS = env_cs;
+      // AREAL_TUNE_K2_CLUSTER_SIZE in {2, 4, 8} forces a larger vocab split
+      const int64_t force = tuning(AREAL_TUNE_K2_CLUSTER_SIZE);
+      if (force > CS) CS = (int)force;
     }
     // A row too long for one CTA's shared memory but within shared memory + TMEM
     // runs on the single-CTA TMEM kernel (no cluster split) unless disabled.
     if constexpr (sizeof(T) == 2 || sizeof(T) == 4) {
-      static const bool tmem_off = [] {
-        const char* s = getenv("AREAL_K2_TMEM");
-        return s && atoi(s) == 0;
-      }();
+      const bool tmem_off = tuning(AREAL_TUNE_K2_TMEM) == 0;
       const int64_t row_chunks = (V16 * 16 + kChunkBytes - 1) / kChunkBytes;
       // rows beyond TMEM + the ring stream their middle chunks (ppo_tmem.cuh)
-      static const bool stream_off = [] {
-        const char* s = getenv("AREAL_K2_TMEM_STREAM");
-        return s && atoi(s) == 0;
-      }();
+      const bool stream_off = tuning(AREAL_TUNE_K2_TMEM_STREAM) == 0;
       // 16-bit rows that fit the ring also run faster on the TMEM kernel (e-form
       // pass 2, longer lookahead): bf16 V = 32,000 5.83 -> 6.51 TB/s, V = 65,536
       // 5.95 -> 6.65; fp32 rows that fit stay on the ring (V = 32,000: 6.67 vs 6.39)
@@ -870,10 +860,8 @@ static bool ring_ok(const void* base, int64_t ld_bytes, int64_t vocab, int es) {
 }
 
 static bool tmem_unaligned_ok(const PpoArgs& a, int es) {
-  static const bool off = [] {  // AREAL_K2_TMEM_UNALIGNED=0: unaligned rows on the row-CTA kernel
-    const char* s = getenv("AREAL_K2_TMEM_UNALIGNED");
-    return s && atoi(s) == 0;
-  }();
+  // AREAL_TUNE_K2_TMEM_UNALIGNED = 0: unaligned rows on the row-CTA kernel
+  const bool off = tuning(AREAL_TUNE_K2_TMEM_UNALIGNED) == 0;
   if (off || a.dlogits == nullptr) return false;
   const int64_t rb = a.vocab * es;
   if (rb < 16384) return false;
@@ -883,29 +871,14 @@ static bool tmem_unaligned_ok(const PpoArgs& a, int es) {
   return (lo + kChunkBytes - 1) / kChunkBytes == (hi + kChunkBytes - 1) / kChunkBytes;
 }
 
-static bool k1_unal_off() {  // AREAL_K1_RING_UNALIGNED=0: unaligned K1 rows on the row-CTA kernel
-  static const bool off = [] {
-    const char* s = getenv("AREAL_K1_RING_UNALIGNED");
-    return s && atoi(s) == 0;
-  }();
-  return off;
-}
+// AREAL_TUNE_K1_RING_UNALIGNED = 0: unaligned K1 rows on the row-CTA kernel
+static bool k1_unal_off() { return tuning(AREAL_TUNE_K1_RING_UNALIGNED) == 0; }
 
-static int64_t small_rowcta_kb() {  // K2 rows up to this many KB on the short-row kernel
-  static const int64_t kb = [] {
-    const char* s = getenv("AREAL_K2_SMALL_ROWCTA_KB");  // -1 / unset: the default rule
-    return s ? (int64_t)atoi(s) : (int64_t)-1;
-  }();
-  return kb;
-}
+// K2 rows up to this many KB on the short-row kernel (-1: the default rule)
+static int64_t small_rowcta_kb() { return tuning(AREAL_TUNE_K2_SMALL_ROWCTA_KB); }
 
-static bool rowcta_off() {  // AREAL_ROWCTA=0: unaligned rows on the one-warp kernel
-  static const bool off = [] {
-    const char* s = getenv("AREAL_ROWCTA");
-    return s && atoi(s) == 0;
-  }();
-  return off;
-}
+// AREAL_TUNE_ROWCTA = 0: unaligned rows on the one-warp kernel
+static bool rowcta_off() { return tuning(AREAL_TUNE_ROWCTA) == 0; }
 
 template <bool BWD>
 static int dispatch(PpoArgs a, int dtype, int algo, cudaStream_t stream) {

@@ -7,6 +7,7 @@ synchronises except ``MicrobatchPlan``-style host reads done by callers.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes
 from dataclasses import dataclass
 
@@ -53,6 +54,32 @@ class _HostStage:
         self.event.record()
         return [dev[o:o + a.nbytes].view(torch.from_numpy(a[:0]).dtype)
                 for a, o in zip(arrays, offs)]
+
+
+def set_tuning(knob: str, value: int) -> int:
+    """Override one kernel-selection rule (areal_set_tuning; include/areal_b200.h
+    areal_tune_t).  ``value`` -1 restores the shipped rule.  Returns the previous value."""
+    lib = _lib.load()
+    if knob not in _lib.TUNE_KNOBS:
+        raise ValueError(f"unknown tuning knob {knob!r}; known: {sorted(_lib.TUNE_KNOBS)}")
+    k = _lib.TUNE_KNOBS[knob]
+    old = ctypes.c_int64()
+    check(lib.areal_get_tuning(k, ctypes.byref(old)), "areal_get_tuning")
+    check(lib.areal_set_tuning(k, int(value)), f"areal_set_tuning({knob}={value})")
+    return int(old.value)
+
+
+@contextlib.contextmanager
+def tuning(**knobs):
+    """``with tuning(k2_tmem=0): ...`` — scoped kernel-selection overrides (A/B, tests)."""
+    prev = {}
+    try:
+        for k, v in knobs.items():
+            prev[k] = set_tuning(k, v)
+        yield
+    finally:
+        for k, v in prev.items():
+            set_tuning(k, v)
 
 
 def _upload(arrays, device):

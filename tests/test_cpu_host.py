@@ -75,6 +75,30 @@ def test_library_validates_without_gpu():
     assert lib.areal_linear_logprob_scratch_bytes(1000, 151936) == 1000 * 149 * 2 * 16
 
 
+def test_tuning_api_validates_and_restores():
+    """Kernel-selection overrides go through areal_set_tuning (nothing is read from the
+    environment); bad knobs / values are rejected; the scoped helper restores defaults."""
+    from paper_2505_24298_b200 import _lib, kernels as K
+    with open(os.path.join(ROOT, "include", "areal_b200.h")) as f:
+        hdr = f.read()
+    for name, code in _lib.TUNE_KNOBS.items():
+        assert re.search(rf"AREAL_TUNE_{name.upper()}\s*=\s*{code},", hdr), name
+    for src in ("ppo_kernels.cu", "linear_lp.cu", "ppo_ring.cuh", "ppo_tmem.cuh", "capi.cu"):
+        with open(os.path.join(ROOT, "paper_2505_24298_b200", "csrc", src)) as f:
+            assert "getenv" not in f.read(), src
+    with pytest.raises(ValueError):
+        K.set_tuning("no_such_knob", 1)
+    with pytest.raises(_lib.ArealError):
+        K.set_tuning("k2_cluster_size", 3)
+    with pytest.raises(_lib.ArealError):
+        K.set_tuning("k7_group", 0)
+    assert _lib.load().areal_set_tuning(99, 0) == _lib.ERR_INVALID_ARGUMENT
+    with K.tuning(k2_tmem=0, k7_nt=4):
+        assert K.set_tuning("k2_tmem", 0) == 0
+        assert K.set_tuning("k7_nt", 4) == 4
+    assert K.set_tuning("k2_tmem", -1) == -1 and K.set_tuning("k7_nt", -1) == -1
+
+
 def test_minibatch_items_matches_reference_split():
     from paper_2505_24298_b200.trainer import minibatch_items
     rng = np.random.default_rng(3)

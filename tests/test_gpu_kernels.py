@@ -147,31 +147,17 @@ def test_ppo_masks_and_scale(algo):
     check_k2("f32", dl, st, ref, T)
 
 
-@pytest.mark.parametrize("env", [{"AREAL_K2_TMEM": "0"}, {"AREAL_CLUSTER_SIZE": "4"}])
-def test_ppo_cluster_variants_bf16(tmp_path, env):
+@pytest.mark.parametrize("knobs", [{"k2_tmem": 0}, {"k2_cluster_size": 4}])
+def test_ppo_cluster_variants_bf16(knobs):
     """The 2-CTA (default when TMEM is off) and 4-CTA cluster splits of K2 (DSMEM
-    exchange of the row statistics) stay correct; knobs are read once per process."""
-    import os
-    import subprocess
-    import sys
+    exchange of the row statistics) stay correct; selected through areal_set_tuning."""
     T, V = 96, 151936
     logits, x64, tokens, behav, prox, adv = make_case(T, V, "bf16", seed=33)
-    np.savez(tmp_path / "in.npz", logits=logits.view(torch.int16).numpy(), tokens=tokens,
-             behav=behav, prox=prox, adv=adv)
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    code = f"""
-import numpy as np, torch, sys
-sys.path.insert(0, {root!r})
-from paper_2505_24298_b200 import kernels as K
-z = np.load({str(tmp_path / 'in.npz')!r})
-lg = torch.from_numpy(z['logits']).view(torch.bfloat16).cuda()
-c = lambda k: torch.from_numpy(z[k]).cuda()
-dl, st = K.ppo_fwd_bwd(lg, c('tokens'), c('behav'), c('prox'), c('adv'), algo='ring')
-np.savez({str(tmp_path / 'out.npz')!r}, dl=dl.double().cpu().numpy(), st=st.cpu().numpy())
-"""
-    subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **env), check=True,
-                   timeout=300)
-    out = np.load(tmp_path / "out.npz")
+    with K.tuning(**knobs):
+        dl, st = K.ppo_fwd_bwd(cuda(logits), cuda(tokens), cuda(behav), cuda(prox), cuda(adv),
+                               algo="ring")
+        torch.cuda.synchronize()
+    out = dict(dl=dl.double().cpu().numpy(), st=st.cpu().numpy())
     ref = O.surrogate_terms(x64, tokens, behav, prox, adv)
     check_k2("bf16", out["dl"], out["st"], ref, T)
 

@@ -12,7 +12,15 @@ ap.add_argument("--dtype", default="bf16")
 ap.add_argument("--iters", type=int, default=10)
 ap.add_argument("--algo", default="auto")
 ap.add_argument("--which", default="k1,k2")
+ap.add_argument("--lib", default=None, help="a tuning build from tools/variants.py")
+ap.add_argument("--tune", action="append", default=[], help="knob=value (areal_set_tuning)")
 a = ap.parse_args()
+if a.lib:
+    from paper_2505_24298_b200 import _lib
+    _lib.use_library(a.lib)
+for kv in a.tune:
+    k_, v_ = kv.split("=")
+    K.set_tuning(k_, int(v_))
 dt = {"bf16": torch.bfloat16, "f32": torch.float32, "f16": torch.float16, "f64": torch.float64}[a.dtype]
 dev = torch.device("cuda", 0)
 T, V = a.rows, a.vocab

@@ -1,8 +1,8 @@
 """Build tuning variants of libareal_b200.so (compile-time knobs) into build/variants/.
 
     python tools/variants.py NAME=-DFLAG=VAL[,-DFLAG2=VAL] ...
-Each variant is selected at run time with AREAL_B200_LIB=build/variants/libareal_b200_NAME.so
-(tools/kbench.py honours it through paper_2505_24298_b200._lib)."""
+Each variant is selected with `tools/kbench.py --lib build/variants/libareal_b200_NAME.so`
+(paper_2505_24298_b200._lib.use_library before the first load).."""
 import os
 import sys
 
