@@ -243,6 +243,23 @@ int areal_linear_logprob_fwd(const void* hidden, int64_t ld_hidden, const void* 
                              const int32_t* row_index, double* lp_out, double* entropy_out,
                              void* scratch, size_t scratch_bytes, int cta_group, void* stream);
 
+/* ---- behaviour log-prob recording at emission ------------------------------
+ * Replaces the per-token record of RolloutWorker.step (rollout.py:154-159:
+ * tokens.append(token); behavior_logprobs.append(P.log_prob(params, features,
+ * token)); versions.append(params.version)) for one decode step of n_rows live
+ * sequences.  Row r belongs to slot slots[r] (distinct within a step); its token
+ * and *version (device int32: graph-capturable) are appended at position lengths[slot]++ of that slot's row in
+ * tok_buf / ver_buf ([n_slots * max_len + 1]; the last entry is a sink), and
+ * row_index_out[r] receives the flat position, so a following
+ * areal_logprob_fwd / areal_linear_logprob_fwd(tokens = tok_buf, row_index =
+ * row_index_out, lp_out = lp_buf) writes the log-prob beside them.  A bad slot
+ * or a full slot sends the row to the sink and raises *status (device int32,
+ * atomicMax of AREAL_ERR_BAD_SHAPE / AREAL_ERR_LEN_EXCEEDS_CAPACITY). */
+int areal_emission_append(const int32_t* slots, const int64_t* step_tokens, int64_t n_rows,
+                          const int32_t* version, int32_t n_slots, int64_t max_len, int32_t* lengths,
+                          int64_t* tok_buf, int32_t* ver_buf, int32_t* row_index_out,
+                          int32_t* status, void* stream);
+
 /* ---- K6: fused global-norm clip + Adam (decoupled weight decay), multi-tensor --
  * Replaces the optimizer step of train_step (trainer.py:329-331): grad.scale_(-1/n)
  * then apply_update (policy.py:225-258) with clip_by_global_norm (policy.py:215-221).

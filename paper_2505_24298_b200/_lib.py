@@ -98,6 +98,8 @@ _SIGS = {
     "areal_linear_logprob_fwd": ([c_vp, c_i64, c_vp, c_i64, c_vp, ctypes.c_int, c_i64, c_i64, c_i64,
                                   c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, ctypes.c_int, c_vp],
                                  ctypes.c_int),
+    "areal_emission_append": ([c_vp, c_vp, c_i64, c_vp, c_i32, c_i64, c_vp, c_vp, c_vp, c_vp,
+                               c_vp, c_vp], ctypes.c_int),
     "areal_adam_step": ([ctypes.POINTER(AdamTensor), c_i32, ctypes.c_int, ctypes.c_int,
                          ctypes.POINTER(AdamParams), c_vp, c_vp, c_sz, c_vp], ctypes.c_int),
 }

@@ -16,6 +16,28 @@
 
 namespace areal {
 
+// Leaf of numpy's pairwise sum (n <= 128): no recursion, so it inlines without a stack.
+template <typename F>
+__device__ __forceinline__ double pw_leaf_f(const F& f, int64_t off, int64_t n) {
+  if (n < 8) {
+    double res = 0.0;
+    for (int64_t i = 0; i < n; ++i) res = __dadd_rn(res, f(off + i));
+    return res;
+  }
+  double r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = f(off + j);
+  int64_t i = 8;
+  for (; i < n - (n % 8); i += 8) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], f(off + i + j));
+  }
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (; i < n; ++i) res = __dadd_rn(res, f(off + i));
+  return res;
+}
+
 // Sum of f(off) .. f(off + n - 1) in numpy's pairwise order.  F: double f(int64_t).
 template <typename F>
 __device__ double pw_sum_f(const F& f, int64_t off, int64_t n) {

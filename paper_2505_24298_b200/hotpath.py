@@ -347,7 +347,11 @@ class DecoupledPPOStep:
         adv = K.advantages(ro.rewards, ro.traj_bounds, ro.n_tokens, mode=c.adv_mode,
                            gamma=c.gamma, lam=c.lam, values=ro.values, norm=norm,
                            group_ids=ro.group_ids, eps=c.adv_eps)
-        self.launches += 1 + (5 if norm == "global" else (1 if norm.startswith("group") else 0))
+        # global norm: one fused cooperative launch (+ the GAE scan before it)
+        if norm == "global":
+            self.launches += 1 if c.adv_mode == "reference" else 2
+        else:
+            self.launches += 1 + (1 if norm.startswith("group") else 0)
         return adv
 
     # ---- K4 + K5
@@ -546,7 +550,8 @@ def emission_logprobs(tokens: torch.Tensor, logits: torch.Tensor | None = None,
     of each sampled token under the generating params), for one decode step of a
     batch of sequences.  Either the step's logits [B, V] (K1) or the final hidden
     states [B, d] + LM head [V, d] (+ bias) (K7, no logits) are given.  Returns
-    float64 [B] — the ``behavior_logprobs`` entries appended to each trajectory."""
+    float64 [B].  ``EmissionRecorder`` keeps whole trajectories (tokens, log-probs,
+    versions) on the device."""
     if (logits is None) == (hidden is None):
         raise ValueError("pass exactly one of logits or hidden (+ weight)")
     if logits is not None:
@@ -556,6 +561,93 @@ def emission_logprobs(tokens: torch.Tensor, logits: torch.Tensor | None = None,
         raise ValueError("hidden needs the LM-head weight")
     lp, _ = K.linear_logprob_fwd(hidden, weight, tokens, bias=bias)
     return lp
+
+
+class EmissionRecorder:
+    """Device-resident provenance record of live sequences: RolloutWorker.step
+    (rollout.py:140-165) appends, per emitted token, the token, its behaviour
+    log-prob ``P.log_prob(params, features, token)`` and ``params.version`` to the
+    sequence's Trajectory (``tokens``, ``behavior_logprobs``, ``versions``).
+
+    ``step(slots, tokens, version, logits=... | hidden=..., weight=...)`` records one
+    decode step of len(slots) sequences in 2 launches (areal_emission_append, then K1
+    or K7 writing the log-probs in place through the row map), with no host sync; the
+    version lives on the device (``set_version``), so with version=None a step can be
+    captured once in a CUDA graph and replayed.
+    ``trajectory(slot)`` returns the three lists' arrays for that slot (one D2H copy),
+    ``release(slot)`` empties it for the next request.  Slots in one step must be
+    distinct; overflow (more than ``max_len`` tokens) or a bad slot is reported by
+    ``check()`` / ``trajectory()`` as the reference's worker would refuse the step.
+    """
+
+    def __init__(self, n_slots: int, max_len: int, device=None):
+        if n_slots < 1 or max_len < 1:
+            raise ValueError("n_slots and max_len must be >= 1")
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.device, self.n_slots, self.max_len = dev, int(n_slots), int(max_len)
+        n = self.n_slots * self.max_len + 1  # + the sink entry
+        self.tokens = torch.zeros(n, dtype=torch.int64, device=dev)
+        self.versions = torch.zeros(n, dtype=torch.int32, device=dev)
+        self.logprobs = torch.zeros(n, dtype=torch.float64, device=dev)
+        self.lengths = torch.zeros(self.n_slots, dtype=torch.int32, device=dev)
+        self.status = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.version = torch.zeros(1, dtype=torch.int32, device=dev)  # generating params' version
+        self._version_host = 0
+        self._rows = torch.empty(0, dtype=torch.int32, device=dev)
+        self.launches = 0
+
+    def set_version(self, version: int) -> None:
+        """update_weights (rollout.py:180-208): later emissions record ``version``."""
+        if int(version) != self._version_host:
+            self.version.fill_(int(version))
+            self._version_host = int(version)
+
+    def step(self, slots: torch.Tensor, tokens: torch.Tensor, version: int | None = None, *,
+             logits: torch.Tensor | None = None, hidden: torch.Tensor | None = None,
+             weight: torch.Tensor | None = None, bias: torch.Tensor | None = None) -> None:
+        if (logits is None) == (hidden is None):
+            raise ValueError("pass exactly one of logits or hidden (+ weight)")
+        B = slots.numel()
+        if tokens.numel() != B:
+            raise ValueError("one sampled token per slot")
+        if slots.dtype != torch.int32 or tokens.dtype != torch.int64:
+            raise TypeError("slots int32, tokens int64")
+        if self._rows.numel() < B:
+            self._rows = torch.empty(B, dtype=torch.int32, device=self.device)
+        rows = self._rows[:B]
+        if version is not None:
+            self.set_version(version)
+        lib = K._lib.load()
+        K.check(lib.areal_emission_append(
+            K._ptr(slots), K._ptr(tokens), B, K._ptr(self.version), self.n_slots, self.max_len,
+            K._ptr(self.lengths), K._ptr(self.tokens), K._ptr(self.versions), K._ptr(rows),
+            K._ptr(self.status), K._stream()), "areal_emission_append")
+        if logits is not None:
+            K.logprob_fwd(logits, self.tokens, row_index=rows, lp_out=self.logprobs,
+                          with_entropy=False)
+            self.launches += 2
+        else:
+            if weight is None:
+                raise ValueError("hidden needs the LM-head weight")
+            K.linear_logprob_fwd(hidden, weight, self.tokens, bias=bias, row_index=rows,
+                                 lp_out=self.logprobs)
+            self.launches += 3
+
+    def check(self) -> None:
+        st = int(self.status.item())
+        if st != 0:
+            raise K._lib.ArealError(st, "EmissionRecorder.step")
+
+    def trajectory(self, slot: int):
+        """(tokens int64, behavior_logprobs float64, versions int32) of ``slot``."""
+        self.check()
+        n = int(self.lengths[slot].item())
+        lo = slot * self.max_len
+        return (self.tokens[lo:lo + n].cpu().numpy(), self.logprobs[lo:lo + n].cpu().numpy(),
+                self.versions[lo:lo + n].cpu().numpy())
+
+    def release(self, slot: int) -> None:
+        self.lengths[slot] = 0
 
 
 def linear_ppo_fwd_bwd(hidden: torch.Tensor, weight: torch.Tensor, tokens: torch.Tensor,

@@ -154,7 +154,7 @@ def test_ppo_cluster_variants_bf16(knobs):
     T, V = 96, 151936
     logits, x64, tokens, behav, prox, adv = make_case(T, V, "bf16", seed=33)
     with K.tuning(**knobs):
-        dl, st = K.ppo_fwd_bwd(cuda(logits), cuda(tokens), cuda(behav), cuda(prox), cuda(adv),
+        dl, st = K.ppo_fwd_bwd(logits.cuda(), cuda(tokens), cuda(behav), cuda(prox), cuda(adv),
                                algo="ring")
         torch.cuda.synchronize()
     out = dict(dl=dl.double().cpu().numpy(), st=st.cpu().numpy())
@@ -270,6 +270,32 @@ def test_advantages_reference_large_bit_exact(T_scale):
     for rewards in (rng.choice([5.0, -5.0], size=len(lengths)), rng.normal(size=len(lengths))):
         adv = K.advantages(cuda(rewards), cuda(bounds), int(bounds[-1]))
         assert np.array_equal(adv.cpu().numpy(), O.compute_advantages_ref(rewards, bounds))
+
+
+@pytest.mark.parametrize("n_traj,lo,hi", [(7, 0, 9), (300, 0, 40), (4096, 64, 600),
+                                           (5000, 0, 700), (600, 6000, 10000)])
+def test_advantages_fused_global_edges(n_traj, lo, hi):
+    """The fused cooperative K3 (one launch) across its regimes: tiny batches (tree depth
+    0-2), empty trajectories anywhere (including first / last), bounds staged in shared
+    memory (<= 4096 trajectories) or read from global memory (5000), and T > 128 * 2^15
+    (leaves > 128 elements: numpy's recursive split inside a leaf).  Bit-exact, plus the
+    returns / norm_stats side outputs."""
+    rng = np.random.default_rng(n_traj)
+    lengths = rng.integers(lo, hi, size=n_traj)
+    lengths[0] = 0
+    lengths[-1] = 0
+    bounds = np.concatenate([[0], np.cumsum(lengths)])
+    T = int(bounds[-1])
+    for rewards in (rng.choice([5.0, -5.0], size=n_traj), rng.normal(size=n_traj) * 3.7,
+                    np.full(n_traj, 0.1)):
+        ret = torch.empty(T, dtype=torch.float64, device="cuda")
+        ns = torch.zeros(2, dtype=torch.float64, device="cuda")
+        adv = K.advantages(cuda(rewards), cuda(bounds), T, returns_out=ret, norm_stats=ns)
+        ref = O.compute_advantages_ref(rewards, bounds)
+        assert np.array_equal(adv.cpu().numpy(), ref)
+        raw = np.repeat(rewards, lengths)
+        assert np.array_equal(ret.cpu().numpy(), raw)
+        assert ns.cpu().numpy().tolist() == [float(np.mean(raw)), float(np.std(raw))]
 
 
 def test_advantages_gae_and_group():

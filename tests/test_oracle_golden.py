@@ -277,3 +277,39 @@ def test_adam_oracle_bit_exact_vs_reference_golden():
             assert step == int(c[f"step{k}"])
         for got, key in ((W, "W"), (b, "b"), (m_w, "mw"), (v_w, "vw"), (m_b, "mb"), (v_b, "vb")):
             assert np.array_equal(got, c[key]), key
+
+
+def test_pairwise_cut_depth_nodes_split_at_most_once():
+    """K3's fused kernel (advantages.cu) cuts numpy's pairwise tree at the depth where the
+    smallest node is <= 128 and relies on every node there being <= 143, i.e. split by numpy
+    at most once more into two <= 128 leaves.  Checked over small n exhaustively and over
+    large n around every power-of-two boundary."""
+    def split(n):
+        n2 = n // 2
+        return n2 - n2 % 8, n - (n2 - n2 % 8)
+
+    def depth(n, cap=20):
+        d = 0
+        while d < cap and n > 128:
+            n, d = split(n)[0], d + 1
+        return d
+
+    def extremes(n, d):  # (smallest, largest) node at depth d: leftmost / rightmost paths
+        lo = hi = n
+        for _ in range(d):
+            lo, hi = split(lo)[0], split(hi)[1]
+        return lo, hi
+
+    rng = np.random.default_rng(0)
+    cases = list(range(1, 20000)) + [int(x) for x in rng.integers(1, 128 << 20, 3000)] + \
+        [(128 << k) + j for k in range(21) for j in range(-40, 41)]
+    for n in cases:
+        if n < 1 or n > (128 << 20):
+            continue
+        d = depth(n)
+        lo, hi = extremes(n, d)
+        assert lo <= 128 and hi <= 143, (n, d, lo, hi)
+        if d > 0:
+            assert extremes(n, d - 1)[0] > 128  # every node above the cut splits
+        if hi > 128:
+            assert max(split(hi)) <= 128
