@@ -139,7 +139,9 @@ typedef enum {
   AREAL_TUNE_ROWCTA = 6,             /* 0: unaligned rows on the one-warp kernel        */
   AREAL_TUNE_K7_NT = 7,              /* {4,8}: K7 N-tiles per unit                      */
   AREAL_TUNE_K7_GROUP = 8,           /* [1,16]: K7 vocab blocks per token tile          */
-  AREAL_TUNE_COUNT = 9
+  AREAL_TUNE_K1_CLUSTER_SIZE = 9,    /* {1,2,4,8}: K1 ring row split (default: by rows) */
+  AREAL_TUNE_LMH_GROUP_M = 10,       /* [1,256]: LM-head GEMM M-tiles per raster group  */
+  AREAL_TUNE_COUNT = 11
 } areal_tune_t;
 #define AREAL_TUNE_DEFAULT (-1)
 int areal_set_tuning(int knob, int64_t value);
@@ -242,6 +244,41 @@ int areal_linear_logprob_fwd(const void* hidden, int64_t ld_hidden, const void* 
                              int64_t vocab, int64_t dim, const int64_t* tokens,
                              const int32_t* row_index, double* lp_out, double* entropy_out,
                              void* scratch, size_t scratch_bytes, int cta_group, void* stream);
+
+/* ---- LM-head GEMMs of the loss + backward (tcgen05) -------------------------
+ * The model side of _surrogate_terms (trainer.py:163, 183-184): logits =
+ * features W^T + b, grad_w = resid^T features, grad_b = sum(resid), for an LM head
+ * W [V, d] over hidden states H [T, d] (16-bit; fp32 accumulation in TMEM).  With
+ * K2 turning a logits chunk into dlogits dL in place, one micro-batch chunk is
+ *   AREAL_LMH_LOGITS   C[M=T, N=V] (16-bit) = A[T, d] B[V, d]^T + bias[V]   (K = d)
+ *   AREAL_LMH_DHIDDEN  C[M=T, N=d] (16-bit) = A[T, V] B[V, d]               (K = V)
+ *   AREAL_LMH_DWEIGHT  C[M=V, N=d] (fp32, += if accumulate) = A[T, V]^T B[T, d]
+ *                                                                           (K = T)
+ * (row-major operands with row strides lda / ldb / ldc elements, 16-byte aligned,
+ * strides multiples of 16 bytes; bias fp32 [N] or NULL, LOGITS only), and
+ * areal_colsum gives grad_b (+)= column sums of dL.  dtype: AREAL_BF16 / AREAL_F16
+ * for A, B and the 16-bit outputs.  Stream-ordered; no allocation. */
+typedef enum { AREAL_LMH_LOGITS = 0, AREAL_LMH_DHIDDEN = 1, AREAL_LMH_DWEIGHT = 2 } areal_lmh_op_t;
+int areal_lm_head_gemm(int op, const void* A, int64_t lda, const void* B, int64_t ldb, void* C,
+                       int64_t ldc, int64_t M, int64_t N, int64_t K, const float* bias,
+                       int accumulate, int dtype, void* stream);
+/* The chunk's whole backward through the head in ONE launch (grouped GEMM: the
+ * DHIDDEN units, then the DWEIGHT units filling the first's last wave), with grad_b
+ * summed from the dlogits tiles while DWEIGHT holds them in shared memory:
+ *   grad_hidden[n_rows, dim] (16-bit)  = dL[n_rows, vocab] W[vocab, dim]
+ *   grad_weight[vocab, dim] (fp32)    (+)= dL^T hidden[n_rows, dim]
+ *   grad_bias[vocab] (fp32, may be NULL) (+)= sum_r dL[r, :]
+ * (+= when accumulate; deterministic).  trainer.py:183-184. */
+int areal_lm_head_backward(const void* dlogits, int64_t ld_dlogits, const void* hidden,
+                           int64_t ld_hidden, const void* weight, int64_t ld_weight,
+                           int64_t n_rows, int64_t vocab, int64_t dim, void* grad_hidden,
+                           int64_t ld_grad_hidden, float* grad_weight, int64_t ld_grad_weight,
+                           float* grad_bias, int accumulate, int dtype, void* stream);
+/* out[c] (+)= sum_r x[r, c] in fp32, deterministic (fixed-order block partials in
+ * `scratch`, areal_colsum_scratch_bytes(rows, cols) bytes). */
+size_t areal_colsum_scratch_bytes(int64_t rows, int64_t cols);
+int areal_colsum(const void* x, int64_t ld, int64_t rows, int64_t cols, int dtype, float* out,
+                 int accumulate, void* scratch, size_t scratch_bytes, void* stream);
 
 /* ---- behaviour log-prob recording at emission ------------------------------
  * Replaces the per-token record of RolloutWorker.step (rollout.py:154-159:

@@ -73,8 +73,10 @@ ADAM_MAX_TENSORS = 32
 # areal_tune_t (kernel-selection overrides; -1 = the shipped rule)
 TUNE_KNOBS = {"k2_cluster_size": 0, "k2_tmem": 1, "k2_tmem_stream": 2, "k2_tmem_unaligned": 3,
               "k1_ring_unaligned": 4, "k2_small_rowcta_kb": 5, "rowcta": 6, "k7_nt": 7,
-              "k7_group": 8}
+              "k7_group": 8, "k1_cluster_size": 9, "lmh_group_m": 10}
 TUNE_DEFAULT = -1
+
+LMH_OPS = {"logits": 0, "dhidden": 1, "dweight": 2}  # areal_lmh_op_t
 
 _SIGS = {
     "areal_abi_version": ([], c_i32),
@@ -98,6 +100,13 @@ _SIGS = {
     "areal_linear_logprob_fwd": ([c_vp, c_i64, c_vp, c_i64, c_vp, ctypes.c_int, c_i64, c_i64, c_i64,
                                   c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, ctypes.c_int, c_vp],
                                  ctypes.c_int),
+    "areal_lm_head_gemm": ([ctypes.c_int, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_i64, c_i64, c_i64,
+                            c_vp, ctypes.c_int, ctypes.c_int, c_vp], ctypes.c_int),
+    "areal_lm_head_backward": ([c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_i64,
+                                c_vp, c_i64, c_vp, ctypes.c_int, ctypes.c_int, c_vp], ctypes.c_int),
+    "areal_colsum_scratch_bytes": ([c_i64, c_i64], c_sz),
+    "areal_colsum": ([c_vp, c_i64, c_i64, c_i64, ctypes.c_int, c_vp, ctypes.c_int, c_vp, c_sz, c_vp],
+                     ctypes.c_int),
     "areal_emission_append": ([c_vp, c_vp, c_i64, c_vp, c_i32, c_i64, c_vp, c_vp, c_vp, c_vp,
                                c_vp, c_vp], ctypes.c_int),
     "areal_adam_step": ([ctypes.POINTER(AdamTensor), c_i32, ctypes.c_int, ctypes.c_int,

@@ -18,7 +18,7 @@ CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB_NAME = "libareal_b200.so"
 LIB_PATH = os.path.join(HERE, LIB_NAME)
-SOURCES = ["ppo_kernels.cu", "advantages.cu", "microbatch.cu", "adam.cu", "linear_lp.cu", "emission.cu", "capi.cu"]
+SOURCES = ["ppo_kernels.cu", "advantages.cu", "microbatch.cu", "adam.cu", "linear_lp.cu", "lm_head.cu", "emission.cu", "capi.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -26,7 +26,7 @@ extern "C" const char* areal_status_string(int status) {
 }
 
 // ---- kernel-selection overrides (areal_tune_t); -1 everywhere = the shipped rules
-static std::atomic<int64_t> g_tuning[AREAL_TUNE_COUNT] = {-1, -1, -1, -1, -1, -1, -1, -1, -1};
+static std::atomic<int64_t> g_tuning[AREAL_TUNE_COUNT] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
 
 int64_t areal::tuning(int knob) {
   return (knob >= 0 && knob < AREAL_TUNE_COUNT) ? g_tuning[knob].load(std::memory_order_relaxed) : -1;
@@ -44,6 +44,8 @@ static bool tuning_valid(int knob, int64_t v) {
     case AREAL_TUNE_K2_SMALL_ROWCTA_KB: return v >= 0 && v <= 1024;
     case AREAL_TUNE_K7_NT: return v == 4 || v == 8;
     case AREAL_TUNE_K7_GROUP: return v >= 1 && v <= 16;
+    case AREAL_TUNE_K1_CLUSTER_SIZE: return v == 1 || v == 2 || v == 4 || v == 8;
+    case AREAL_TUNE_LMH_GROUP_M: return v >= 1 && v <= 256;
     default: return false;
   }
 }

@@ -285,6 +285,12 @@ __device__ __forceinline__ void mbar_remote_arrive_release(uint32_t remote_bar) 
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote_bar)
                : "memory");
 }
+// Remote arrive with the default (.release.cta) semantics, as CUTLASS's
+// ClusterBarrier::arrive(cta_id): no global-memory fence, for signals that only order
+// tcgen05 / shared-memory work already fenced by the caller (TMEM slot releases).
+__device__ __forceinline__ void mbar_remote_arrive(uint32_t remote_bar) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(remote_bar) : "memory");
+}
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
                    : "memory");

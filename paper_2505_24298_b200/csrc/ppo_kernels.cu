@@ -27,6 +27,7 @@
 //              row (the bf16 V ~ 152K default).  Unaligned 16/32-bit rows too (UNAL
 //              instantiation: bulk copies from the 16-byte boundary below the row).
 // HBM traffic = one logits read (+ one dlogits write for K2) per element.
+#include <algorithm>
 #include <cstdlib>
 #include <type_traits>
 
@@ -743,6 +744,16 @@ static int launch_ring(PpoArgs a, cudaStream_t stream, int cs_force) {
           (row_chunks <= kTmemMaxChunks || !stream_off))
         return launch_tmem<T, ENT>(a, stream, d, nslots);
     }
+  }
+  if (!BWD && cs_force == 0) {
+    // K1 on few long rows (decode steps): rows that fit one wave of CTA pairs are split
+    // over a 2-CTA cluster (B = 64 x V = 151,936 bf16: 10.2 -> 9.5 us, L2-hot 8.9 -> 7.6 us).
+    // Wider splits and multi-wave splits measured slower (B = 256: CS 1 17.9 us, 2 18.7,
+    // 4 22.9, 8 47.2; profiles/r02_k1_cluster_split.txt): per-row MUFU work and the fixed
+    // launch / pipeline-fill latency bound these shapes, not HBM.
+    const int64_t forced = tuning(AREAL_TUNE_K1_CLUSTER_SIZE);
+    if (forced > 0) CS = (int)forced;
+    else if (a.n_rows <= d.sms / 2 && V16 * 16 >= 4 * (int64_t)kChunkBytes) CS = 2;
   }
   if ((V16 + CS - 1) / CS * 16 > (int64_t)0x7fffffff) return AREAL_ERR_UNSUPPORTED;
   a.cluster_size = CS;

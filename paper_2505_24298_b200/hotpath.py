@@ -660,16 +660,18 @@ def linear_ppo_fwd_bwd(hidden: torch.Tensor, weight: torch.Tensor, tokens: torch
                        grad_weight: torch.Tensor | None = None,
                        grad_bias: torch.Tensor | None = None, algo: str = "auto",
                        prox_from_lp: bool = False, lp_out: torch.Tensor | None = None):
-    """Decoupled-PPO loss + backward THROUGH the LM head, without materialising the
-    micro-batch's [T, V] logits: the rows are processed in chunks of ``chunk_tokens``.
+    """Decoupled-PPO loss + backward THROUGH the LM head on the tensor cores, the
+    micro-batch's rows in chunks of ``chunk_tokens`` (only one chunk's [rows, V] logits
+    exist at a time).
 
-    _surrogate_terms (trainer.py:150-195) including its model GEMMs: per chunk,
-    logits = h W^T + b (cuBLAS bf16, fp32 accumulate) -> K2 in place -> dlogits,
-    then dH = dl W (trainer.py:183's residual^T features, transposed) and
-    dW += dl^T h, db += sum(dl) (trainer.py:183-184) accumulated in fp32.
-    Peak extra memory is chunk_tokens x V x 2 bytes (2.5 GB at 8,192 x 151,936)
-    instead of the full micro-batch's 10 GB.  Fusing the GEMMs into K2 does not pay
-    (DESIGN.md §8): a fused backward must recompute the logits GEMM.
+    _surrogate_terms (trainer.py:150-195) including its model GEMMs, per chunk:
+    logits = h W^T + b (areal_lm_head_gemm LOGITS, tcgen05, fp32 accumulate, bf16 out)
+    -> K2 in place -> dlogits dL, then one grouped launch (areal_lm_head_backward):
+    dH = dL W (trainer.py:183's residual^T features, transposed), dW += dL^T h (fp32,
+    accumulated across chunks in the epilogue) and db += sum(dL) summed from the dL tiles
+    in shared memory (trainer.py:183-184).  Three launches per chunk, all of them this
+    library's kernels.  Peak extra memory is
+    chunk_tokens x V x 2 bytes (2.5 GB at 8,192 x 151,936).
 
     ``prox_from_lp`` / ``lp_out``: as in kernels.ppo_fwd_bwd (first minibatch of a step).
 
@@ -686,31 +688,37 @@ def linear_ppo_fwd_bwd(hidden: torch.Tensor, weight: torch.Tensor, tokens: torch
     V = weight.shape[0]
     if stats is None:
         stats = torch.zeros(K._lib.N_STATS, dtype=torch.float64, device=dev)
-    if grad_weight is None:
-        grad_weight = torch.zeros(V, d, dtype=torch.float32, device=dev)
-    if bias is not None and grad_bias is None:
-        grad_bias = torch.zeros(V, dtype=torch.float32, device=dev)
+    fresh_w = grad_weight is None
+    if fresh_w:
+        grad_weight = torch.empty(V, d, dtype=torch.float32, device=dev)
+    fresh_b = bias is not None and grad_bias is None
+    if fresh_b:
+        grad_bias = torch.empty(V, dtype=torch.float32, device=dev)
     grad_hidden = torch.empty_like(hidden)
-    bias16 = bias.to(hidden.dtype) if bias is not None else None
+    bias32 = bias.float().contiguous() if bias is not None else None
     chunk = max(1, int(chunk_tokens))
-    buf = torch.empty((min(chunk, max(T, 1)), V), dtype=hidden.dtype, device=dev)
+    ldv = (V + 7) // 8 * 8  # 16-byte row stride for the tensor maps
+    buf = torch.empty((min(chunk, max(T, 1)), ldv), dtype=hidden.dtype, device=dev)
+    # one accumulate flag drives grad_w and grad_b: the first chunk may overwrite only
+    # when both are fresh; otherwise fresh ones start from zero
+    acc0 = not fresh_w or (grad_bias is not None and not fresh_b)
+    if (acc0 or T == 0) and fresh_w:
+        grad_weight.zero_()
+    if (acc0 or T == 0) and fresh_b:
+        grad_bias.zero_()
     for lo in range(0, T, chunk):
         hi = min(T, lo + chunk)
         h = hidden[lo:hi]
-        lg = buf[: hi - lo]
-        if bias16 is not None:
-            torch.addmm(bias16, h, weight.t(), out=lg)
-        else:
-            torch.mm(h, weight.t(), out=lg)
+        lg = buf[: hi - lo, :V]
+        K.lm_head_gemm("logits", h, weight, lg, bias=bias32)                    # trainer.py:163
         ri = row_index[lo:hi] if row_index is not None else \
             torch.arange(lo, hi, dtype=torch.int32, device=dev)
         K.ppo_fwd_bwd(lg, tokens, behav, prox, adv, clip_eps=clip_eps, decoupled=decoupled,
                       versions=versions, current_version=current_version, eta_mask=eta_mask,
                       behav_weight_cap=behav_weight_cap, grad_scale=grad_scale, row_index=ri,
                       dlogits=lg, stats=stats, algo=algo, prox_from_lp=prox_from_lp,
-                      lp_out=lp_out)
-        torch.mm(lg, weight, out=grad_hidden[lo:hi])                      # dH = dl W
-        grad_weight.add_(torch.mm(lg.t(), h, out_dtype=torch.float32))   # dW += dl^T h
-        if grad_bias is not None:
-            grad_bias.add_(lg.sum(dim=0, dtype=torch.float32))           # db += sum dl
+                      lp_out=lp_out)                                              # 164-182
+        # dH = dL W, dW (+)= dL^T h, db (+)= sum dL (trainer.py:183-184): one grouped launch
+        K.lm_head_backward(lg, h, weight, grad_hidden[lo:hi], grad_weight, grad_bias,
+                           accumulate=acc0 or lo > 0, with_bias=grad_bias is not None)
     return grad_hidden, grad_weight, grad_bias, stats

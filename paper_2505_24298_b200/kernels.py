@@ -459,3 +459,108 @@ def linear_logprob_fwd(hidden: torch.Tensor, weight: torch.Tensor, tokens: torch
                                        _ptr(scratch), scratch.numel(), int(cta_group), _stream()),
           "areal_linear_logprob_fwd")
     return lp_out, entropy_out
+
+
+# ---------------------------------------------------------------- LM-head GEMMs (tcgen05)
+def _ld(t: torch.Tensor) -> int:
+    """Row stride in elements; a single row's is free, so report it 16-byte rounded."""
+    return t.stride(0) if t.shape[0] > 1 else (t.shape[1] + 7) // 8 * 8
+
+
+def lm_head_gemm(op: str, A: torch.Tensor, B: torch.Tensor, C: torch.Tensor | None = None, *,
+                 bias: torch.Tensor | None = None, accumulate: bool = False) -> torch.Tensor:
+    """The LM head's GEMMs on tcgen05 (areal_lm_head_gemm, lm_head.cu):
+
+    ``"logits"``  C[T, V] = A[T, d] @ B[V, d]^T (+ bias[V])   (16-bit out)
+    ``"dhidden"`` C[T, d] = A[T, V] @ B[V, d]                 (16-bit out)
+    ``"dweight"`` C[V, d] (+)= A[T, V]^T @ B[T, d]            (fp32 out, += if accumulate)
+
+    trainer.py:163 (logits = features W^T + b) and 183-184 (grad_w = resid^T features);
+    fp32 accumulation in Tensor Memory.  Rows must be unit-stride with 16-byte aligned
+    row strides."""
+    lib = _lib.load()
+    if op not in _lib.LMH_OPS:
+        raise ValueError(f"unknown op {op!r}")
+    if A.dim() != 2 or B.dim() != 2 or A.dtype != B.dtype or A.dtype not in (torch.bfloat16, torch.float16):
+        raise TypeError("A and B must be 2-D bfloat16 / float16 tensors of one dtype")
+    if A.device != B.device or (A.numel() and A.stride(1) != 1) or (B.numel() and B.stride(1) != 1):
+        raise ValueError("A and B must be row-major (unit column stride) on one device")
+    dev = A.device
+    if op == "logits":
+        (M, K), (N, K2) = A.shape, B.shape
+        out_dtype = A.dtype
+    elif op == "dhidden":
+        (M, K), (K2, N) = A.shape, B.shape
+        out_dtype = A.dtype
+    else:
+        (K, M), (K2, N) = A.shape, B.shape
+        out_dtype = torch.float32
+    if K != K2:
+        raise ValueError(f"{op}: inner dimensions differ ({K} vs {K2})")
+    if C is None:  # rows padded to 16 bytes (the kernel's vector stores)
+        C = (torch.zeros if accumulate else torch.empty)((M, (N + 7) // 8 * 8), dtype=out_dtype,
+                                                         device=dev)[:, :N]
+    if C.shape != (M, N) or C.dtype != out_dtype or (C.numel() and C.stride(1) != 1):
+        raise ValueError(f"{op}: C must be a row-major {out_dtype} [{M}, {N}] tensor")
+    if bias is not None:
+        if op != "logits":
+            raise ValueError("bias applies to the logits GEMM only")
+        _need(bias, "bias", torch.float32, dev, N)
+    check(lib.areal_lm_head_gemm(_lib.LMH_OPS[op], _ptr(A), _ld(A), _ptr(B), _ld(B), _ptr(C), _ld(C),
+                                 M, N, K, _ptr(bias), int(bool(accumulate)),
+                                 _lib.DTYPE_CODES[A.dtype], _stream()), f"areal_lm_head_gemm({op})")
+    return C
+
+
+def lm_head_backward(dlogits: torch.Tensor, hidden: torch.Tensor, weight: torch.Tensor,
+                     grad_hidden: torch.Tensor | None = None, grad_weight: torch.Tensor | None = None,
+                     grad_bias: torch.Tensor | None = None, accumulate: bool = False, with_bias: bool = True):
+    """One launch for the chunk's backward through the head (areal_lm_head_backward):
+    grad_hidden = dL @ W, grad_weight (+)= dL^T @ hidden, grad_bias (+)= dL.sum(0)
+    (trainer.py:183-184), grouped on tcgen05 with grad_b fused into the DWEIGHT tiles."""
+    lib = _lib.load()
+    for t, nm in ((dlogits, "dlogits"), (hidden, "hidden"), (weight, "weight")):
+        if t.dim() != 2 or (t.numel() and t.stride(1) != 1):
+            raise ValueError(f"{nm} must be a row-major 2-D tensor")
+    if not (dlogits.dtype == hidden.dtype == weight.dtype) or dlogits.dtype not in (torch.bfloat16, torch.float16):
+        raise TypeError("dlogits, hidden and weight must share a 16-bit dtype")
+    T, V = dlogits.shape
+    d = hidden.shape[1]
+    if hidden.shape[0] != T or weight.shape != (V, d):
+        raise ValueError("shapes: dlogits [T, V], hidden [T, d], weight [V, d]")
+    dev = dlogits.device
+    if grad_hidden is None:
+        grad_hidden = torch.empty((T, (d + 7) // 8 * 8), dtype=hidden.dtype, device=dev)[:, :d]
+    if grad_weight is None:
+        grad_weight = (torch.zeros if accumulate else torch.empty)((V, (d + 3) // 4 * 4), dtype=torch.float32,
+                                                                   device=dev)[:, :d]
+    if with_bias and grad_bias is None:
+        grad_bias = (torch.zeros if accumulate else torch.empty)(V, dtype=torch.float32, device=dev)
+    if grad_bias is not None:
+        _need(grad_bias, "grad_bias", torch.float32, dev, V)
+    if grad_hidden.shape != (T, d) or grad_weight.shape != (V, d) or grad_weight.dtype != torch.float32:
+        raise ValueError("grad_hidden [T, d] (hidden dtype) and grad_weight [V, d] fp32")
+    check(lib.areal_lm_head_backward(_ptr(dlogits), _ld(dlogits) if T else V, _ptr(hidden),
+                                     _ld(hidden) if T else d, _ptr(weight), _ld(weight), T, V, d,
+                                     _ptr(grad_hidden), _ld(grad_hidden) if T else d, _ptr(grad_weight),
+                                     _ld(grad_weight), _ptr(grad_bias), int(bool(accumulate)),
+                                     _lib.DTYPE_CODES[dlogits.dtype], _stream()), "areal_lm_head_backward")
+    return grad_hidden, grad_weight, grad_bias
+
+
+def colsum(x: torch.Tensor, out: torch.Tensor | None = None, accumulate: bool = False) -> torch.Tensor:
+    """out[c] (+)= sum_r x[r, c] in fp32, deterministic (areal_colsum): grad_b of the head
+    (trainer.py:184, resid.sum over tokens)."""
+    lib = _lib.load()
+    if x.dim() != 2 or x.dtype not in (torch.bfloat16, torch.float16) or (x.numel() and x.stride(1) != 1):
+        raise TypeError("x must be a row-major 2-D bfloat16 / float16 tensor")
+    rows, cols = x.shape
+    dev = x.device
+    if out is None:
+        out = (torch.zeros if accumulate else torch.empty)(cols, dtype=torch.float32, device=dev)
+    _need(out, "out", torch.float32, dev, cols)
+    scratch = _scratch(dev, int(lib.areal_colsum_scratch_bytes(rows, cols)))
+    check(lib.areal_colsum(_ptr(x), _ld(x) if rows else cols, rows, cols, _lib.DTYPE_CODES[x.dtype],
+                           _ptr(out), int(bool(accumulate)), _ptr(scratch), scratch.numel(), _stream()),
+          "areal_colsum")
+    return out

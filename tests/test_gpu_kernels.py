@@ -71,6 +71,22 @@ def test_logprob_fwd_matches_oracle(dt, V, algo):
     assert np.allclose(ent.cpu().numpy(), ref_ent, rtol=tol, atol=tol * 10)
 
 
+@pytest.mark.parametrize("dt,V", [("bf16", 151936), ("f32", 32000), ("f16", 152064)])
+@pytest.mark.parametrize("cs", [None, 1, 2, 4, 8])
+def test_logprob_few_rows_cluster_split(dt, V, cs):
+    """K1 on decode-step shapes: few long rows are split over a 2/4/8-CTA cluster (DSMEM
+    exchange of the row statistics); the default rule and every forced split agree with
+    the oracle, entropy included."""
+    for T in (1, 3, 64, 200):
+        logits, x64, tokens, *_ = make_case(T, V, dt, seed=T + V)
+        knobs = {} if cs is None else {"k1_cluster_size": cs}
+        with K.tuning(**knobs):
+            lp, ent = K.logprob_fwd(logits.cuda(), cuda(tokens))
+            torch.cuda.synchronize()
+        assert np.allclose(lp.cpu().numpy(), O.token_logprobs(x64, tokens), rtol=1e-5, atol=1e-5)
+        assert np.allclose(ent.cpu().numpy(), O.token_entropy(x64), rtol=1e-5, atol=1e-4)
+
+
 # ---------------------------------------------------------------- K2
 def run_k2(logits, x64, tokens, behav, prox, adv, dt, algo, decoupled=True, eps=0.2, **kw):
     dl, st = K.ppo_fwd_bwd(logits.cuda(), cuda(tokens), cuda(behav), cuda(prox), cuda(adv),

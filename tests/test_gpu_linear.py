@@ -118,9 +118,10 @@ def test_linear_ppo_fwd_bwd_matches_float64_autograd(chunk):
     ratio = torch.exp(lpa - prox)
     obj = scale * torch.minimum(ratio * adv, torch.clamp(ratio, 0.8, 1.2) * adv)
     (-obj.sum()).backward()
-    # (1) tight: the float64 chain rule through the head's own bf16 logits (the same
-    # cuBLAS call), i.e. the restated _surrogate_terms on exactly what K2 sees
-    lg16 = torch.addmm(b.to(torch.bfloat16), h, w.t())
+    # (1) tight: the float64 chain rule through the head's own bf16 logits (the library's
+    # logits GEMM, tested on its own above), i.e. the restated _surrogate_terms on
+    # exactly what K2 sees
+    lg16 = K.lm_head_gemm("logits", h, w, bias=b)
     ref = O.surrogate_terms(lg16.double().cpu().numpy(), tok.cpu().numpy(), behav.cpu().numpy(),
                             prox.cpu().numpy(), adv.cpu().numpy())
     dl = torch.as_tensor(ref["dlogits"], device=DEV)
@@ -186,7 +187,7 @@ def test_linear_ppo_fwd_bwd_row_index_and_prox_from_lp():
     for a, c in zip(outs[0], outs[1]):
         torch.testing.assert_close(a, c, rtol=1e-4, atol=1e-5)
     # prox == the float64 log-softmax of the head's own bf16 logits (what K2 reads)
-    lg16 = torch.addmm(b.to(torch.bfloat16), h, w.t()).double()
+    lg16 = K.lm_head_gemm("logits", h, w, bias=b).double()
     rlp = torch.log_softmax(lg16, 1).gather(1, tok_rows[:, None])[:, 0]
     torch.testing.assert_close(outs[0][4][perm.long()], rlp, rtol=0, atol=1e-4)
     s = outs[0][3].cpu().numpy()
@@ -210,3 +211,121 @@ def test_linear_logprob_fuzz(seed):
     torch.testing.assert_close(lp, rlp, rtol=0, atol=ATOL)
     if ent_on:
         torch.testing.assert_close(ent, rent, rtol=1e-5, atol=ATOL)
+
+
+def _gemm_operands(op, M, N, K, dtype, seed, pad=0):
+    """A, B (row-major, rows padded by `pad` elements) for areal_lm_head_gemm and the
+    float64 reference C."""
+    g = torch.Generator(device=DEV).manual_seed(seed)
+
+    def mat(r, c):  # row stride: c rounded up to 8 elements (16 bytes) + pad
+        full = torch.randn(r, (c + 7) // 8 * 8 + pad, device=DEV, generator=g).to(dtype)
+        return full[:, :c]
+    if op == "logits":
+        A, B = mat(M, K), mat(N, K)
+        ref = A.double() @ B.double().t()
+    elif op == "dhidden":
+        A, B = mat(M, K), mat(K, N)
+        ref = A.double() @ B.double()
+    else:
+        A, B = mat(K, M), mat(K, N)
+        ref = A.double().t() @ B.double()
+    absref = {"logits": lambda: A.double().abs() @ B.double().abs().t(),
+              "dhidden": lambda: A.double().abs() @ B.double().abs(),
+              "dweight": lambda: A.double().abs().t() @ B.double().abs()}[op]()
+    return A, B, ref, absref
+
+
+@pytest.mark.parametrize("op", ["logits", "dhidden", "dweight"])
+@pytest.mark.parametrize("M,N,Kd", [(256, 256, 64), (300, 1000, 128), (1, 7, 64), (517, 333, 200),
+                                    (1024, 1536, 4096), (77, 4096, 1000)])
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+def test_lm_head_gemm_matches_float64(op, M, N, Kd, dtype):
+    """Each tcgen05 GEMM of the head (K-major / MN-major operands, tails of every tile
+    dimension, padded row strides) against float64 matmul of the same 16-bit values:
+    fp32 accumulation error <= 2^-20 x K of the absolute products, plus the output
+    rounding (16-bit outputs: half an ulp)."""
+    A, B, ref, absref = _gemm_operands(op, M, N, Kd, dtype, seed=M + N + Kd, pad=8)
+    bias = torch.randn(N, device=DEV) if op == "logits" else None
+    C = K.lm_head_gemm(op, A, B, bias=bias)
+    if bias is not None:
+        ref = ref + bias.double()
+        absref = absref + bias.double().abs()
+    ulp = 2.0 ** -8 if dtype == torch.bfloat16 else 2.0 ** -11
+    out_round = ulp * ref.abs() if op != "dweight" else 0.0
+    bound = 2.0 ** -20 * Kd * absref + out_round + 1e-30
+    err = (C.double() - ref).abs()
+    assert bool((err <= bound).all()), float((err / bound).max())
+
+
+def test_lm_head_gemm_accumulate_and_strides():
+    """DWEIGHT accumulates into an existing fp32 C (row stride > N); LOGITS writes into a
+    row-strided 16-bit buffer and leaves the padding untouched."""
+    A, B, ref, _ = _gemm_operands("dweight", 300, 200, 129, torch.bfloat16, seed=5)
+    Cbig = torch.ones(300, 208, dtype=torch.float32, device=DEV)
+    C = Cbig[:, :200]
+    K.lm_head_gemm("dweight", A, B, C, accumulate=True)
+    torch.testing.assert_close(C.double(), ref + 1.0, rtol=1e-5, atol=1e-4)
+    assert bool((Cbig[:, 200:] == 1).all())
+    K.lm_head_gemm("dweight", A, B, C, accumulate=False)
+    torch.testing.assert_close(C.double(), ref, rtol=1e-5, atol=1e-4)
+    A, B, ref, _ = _gemm_operands("logits", 70, 1000, 64, torch.bfloat16, seed=6)
+    big = torch.full((70, 1008), 7.0, dtype=torch.bfloat16, device=DEV)
+    K.lm_head_gemm("logits", A, B, big[:, :1000])
+    torch.testing.assert_close(big[:, :1000].double(), ref, rtol=1e-2, atol=1e-2)
+    assert bool((big[:, 1000:] == 7).all())
+
+
+def test_lm_head_gemm_rejects_bad_inputs():
+    a = torch.randn(64, 64, device=DEV).to(torch.bfloat16)
+    with pytest.raises(ValueError):
+        K.lm_head_gemm("logits", a, a[:, :32])  # inner dims differ
+    with pytest.raises(TypeError):
+        K.lm_head_gemm("logits", a.float(), a.float())
+    with pytest.raises(ValueError):
+        K.lm_head_gemm("dhidden", a, a, bias=torch.zeros(64, device=DEV))
+    odd = torch.randn(64, 70, device=DEV).to(torch.bfloat16)[:, :65]  # row stride 140 B
+    with pytest.raises(K._lib.ArealError, match="misaligned"):
+        K.lm_head_gemm("logits", odd, odd)
+
+
+@pytest.mark.parametrize("rows,cols", [(1, 7), (3000, 5000), (4100, 151936), (0, 9)])
+def test_colsum_matches_float64(rows, cols):
+    g = torch.Generator(device=DEV).manual_seed(rows + cols)
+    x = torch.randn(rows, cols, device=DEV, generator=g).to(torch.bfloat16)
+    ref = x.double().sum(0)
+    got = K.colsum(x)
+    assert torch.allclose(got.double(), ref, rtol=1e-5, atol=1e-5 * max(rows, 1) ** 0.5)
+    got2 = K.colsum(x, out=torch.ones(cols, device=DEV), accumulate=True)
+    assert torch.allclose(got2.double(), ref + 1, rtol=1e-5, atol=1e-5 * max(rows, 1) ** 0.5)
+    assert torch.equal(K.colsum(x), got)  # deterministic
+
+
+@pytest.mark.parametrize("T,V,d", [(1, 7, 64), (300, 1000, 128), (517, 2049, 192), (2000, 5000, 256)])
+@pytest.mark.parametrize("accumulate", [False, True])
+def test_lm_head_backward_grouped(T, V, d, accumulate):
+    """areal_lm_head_backward (one grouped launch: DHIDDEN + DWEIGHT, grad_b summed from
+    the shared-memory dL tiles) == the float64 products of the same 16-bit values."""
+    g = torch.Generator(device=DEV).manual_seed(T + V + d)
+    ldv = (V + 7) // 8 * 8  # 16-byte row stride, as the hot path allocates the chunk buffer
+    dl = (torch.randn(T, ldv, device=DEV, generator=g) * 0.1).to(torch.bfloat16)[:, :V]
+    h = torch.randn(T, d, device=DEV, generator=g).to(torch.bfloat16)
+    w = (torch.randn(V, d, device=DEV, generator=g) / d ** 0.5).to(torch.bfloat16)
+    gw0 = torch.randn(V, d, device=DEV, generator=g) if accumulate else None
+    gb0 = torch.randn(V, device=DEV, generator=g) if accumulate else None
+    gw = gw0.clone() if accumulate else None
+    gb = gb0.clone() if accumulate else None
+    dh, gw, gb = K.lm_head_backward(dl, h, w, grad_weight=gw, grad_bias=gb, accumulate=accumulate)
+    rdh = dl.double() @ w.double()
+    rgw = dl.double().t() @ h.double() + (gw0.double() if accumulate else 0)
+    rgb = dl.double().sum(0) + (gb0.double() if accumulate else 0)
+    bound_h = 2.0 ** -20 * V * (dl.double().abs() @ w.double().abs()) + 2.0 ** -8 * rdh.abs() + 1e-30
+    assert bool(((dh.double() - rdh).abs() <= bound_h).all())
+    bound_w = 2.0 ** -20 * T * (dl.double().abs().t() @ h.double().abs()) + 1e-6 * rgw.abs() + 1e-30
+    assert bool(((gw.double() - rgw).abs() <= bound_w).all())
+    bound_b = 2.0 ** -20 * T * dl.double().abs().sum(0) + 1e-6 * rgb.abs() + 1e-30
+    assert bool(((gb.double() - rgb).abs() <= bound_b).all())
+    dh2, gw2, gb2 = K.lm_head_backward(dl, h, w, grad_weight=gw0.clone() if accumulate else None,
+                                       grad_bias=gb0.clone() if accumulate else None,
+                                       accumulate=accumulate)
+    assert torch.equal(dh, dh2) and torch.equal(gw, gw2) and torch.equal(gb, gb2)  # deterministic

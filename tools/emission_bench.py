@@ -4,8 +4,9 @@ rollout.py:154-159): one decode step of B live sequences at V = 151,936 bf16.
     python tools/emission_bench.py [--batches 64,256,1024] [--vocab 151936] [--dim 1536]
 
 Per B it reports, each as CUDA-event time per step over --iters steps:
-  k1_hbm    K1 alone on logits rotated through > L2 of buffers (HBM-resident logits):
-            roofline line, algorithmic bytes B * (V * 2 + 16)
+  k1_hbm    K1 alone on logits rotated through > L2 of buffers (HBM-resident logits),
+            launched from a CUDA graph (device time, no host overhead): roofline line,
+            algorithmic bytes B * (V * 2 + 16); eager_us = the same from Python
   k1_l2hot  K1 on the logits the LM head just wrote (one buffer, L2-resident) — the
             in-engine case, reported without a roofline (L2 is not the HBM bound)
   step      EmissionRecorder.step (append kernel + K1), eager and CUDA-graph replayed
@@ -71,8 +72,32 @@ for B in [int(x) for x in a.batches.split(",")]:
         it[0] = (it[0] + 1) % nbuf
         K.logprob_fwd(bufs[it[0]], tok, lp_out=lp, with_entropy=False)
 
-    us_hbm = timed(k1_rot, a.iters)
-    us_hot = timed(lambda: K.logprob_fwd(bufs[0], tok, lp_out=lp, with_entropy=False), a.iters)
+    us_hbm_eager = timed(k1_rot, a.iters)
+    # device time without the host: G launches over the rotating buffers in one CUDA graph
+    G = 4 * nbuf
+
+    def graph_of(fn):
+        st_ = torch.cuda.Stream()
+        st_.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(st_):
+            fn()
+        torch.cuda.current_stream().wait_stream(st_)
+        torch.cuda.synchronize()
+        g_ = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g_):
+            fn()
+        return g_
+
+    def k1_all():
+        for i in range(G):
+            K.logprob_fwd(bufs[i % nbuf], tok, lp_out=lp, with_entropy=False)
+    gk1 = graph_of(k1_all)
+    us_hbm = timed(gk1.replay, max(3, a.iters // G)) / G
+
+    def k1_hot_all():
+        for i in range(G):
+            K.logprob_fwd(bufs[0], tok, lp_out=lp, with_entropy=False)
+    us_hot = timed(graph_of(k1_hot_all).replay, max(3, a.iters // G)) / G
     by = B * (V * 2 + 16)
     rec = EmissionRecorder(n_slots=B, max_len=a.iters * 4 + 64, device=dev)
     slots = torch.arange(B, dtype=torch.int32, device=dev)
@@ -100,7 +125,8 @@ for B in [int(x) for x in a.batches.split(",")]:
         "metric": "emission log-prob recording, one decode step", "B": B, "vocab": V,
         "dtype": "bf16",
         "k1_hbm": {"us": us_hbm, "gbs": by / us_hbm / 1e3, "frac": by / us_hbm / 1e3 / hbm_peak,
-                   "bytes": by, "rotating_buffers": nbuf},
+                   "bytes": by, "rotating_buffers": nbuf, "timing": "CUDA graph of %d launches" % G,
+                   "eager_us": us_hbm_eager},
         "k1_l2hot": {"us": us_hot, "gbs_effective": by / us_hot / 1e3},
         "step_eager_us": us_step, "step_graph_us": us_graph, "launches_per_step": 2,
         "k7": {"us": us_k7, "dim": d, "weight_gbs": w_bytes / us_k7 / 1e3,
