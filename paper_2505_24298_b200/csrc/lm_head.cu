@@ -404,8 +404,16 @@ __global__ void __launch_bounds__(kind_threads(KIND), 1)
 }
 
 // grad_b = column sums of dL: stage 1 sums row blocks of kColRows rows per (column group of
-// 8, block) into fp32 partials; stage 2 adds the blocks in order (deterministic).
-constexpr int kColRows = 2048;
+// 8, block) into fp32 partials, 4 rows in flight per thread; stage 2 adds the blocks in
+// order (deterministic).
+constexpr int kColRows = 1024;
+
+template <typename T>
+__device__ __forceinline__ void add8(float (&s)[8], const uint4& w) {
+  const T* e = reinterpret_cast<const T*>(&w);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s[i] += (float)e[i];
+}
 
 template <typename T>
 __global__ void colsum_partial_kernel(const T* x, int64_t ld, int64_t rows, int64_t cols, float* part) {
@@ -414,17 +422,23 @@ __global__ void colsum_partial_kernel(const T* x, int64_t ld, int64_t rows, int6
   if (g * 8 >= cols) return;
   const int64_t r0 = blk * kColRows, r1 = r0 + kColRows < rows ? r0 + kColRows : rows;
   float s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  const bool vec = g * 8 + 8 <= cols;
-  for (int64_t r = r0; r < r1; ++r) {
-    const T* p = x + r * ld + g * 8;
-    if (vec) {
-      const uint4 w = __ldg(reinterpret_cast<const uint4*>(p));
-      const T* e = reinterpret_cast<const T*>(&w);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) s[i] += (float)e[i];
-    } else {
-      for (int i = 0; g * 8 + i < cols; ++i) s[i] += (float)p[i];
+  if (g * 8 + 8 <= cols) {
+    const T* p = x + r0 * ld + g * 8;
+    int64_t r = r0;
+    for (; r + 4 <= r1; r += 4, p += 4 * ld) {  // 4 independent 16-byte loads in flight
+      const uint4 w0 = __ldg(reinterpret_cast<const uint4*>(p));
+      const uint4 w1 = __ldg(reinterpret_cast<const uint4*>(p + ld));
+      const uint4 w2 = __ldg(reinterpret_cast<const uint4*>(p + 2 * ld));
+      const uint4 w3 = __ldg(reinterpret_cast<const uint4*>(p + 3 * ld));
+      add8<T>(s, w0);
+      add8<T>(s, w1);
+      add8<T>(s, w2);
+      add8<T>(s, w3);
     }
+    for (; r < r1; ++r, p += ld) add8<T>(s, __ldg(reinterpret_cast<const uint4*>(p)));
+  } else {
+    for (int64_t r = r0; r < r1; ++r)
+      for (int i = 0; g * 8 + i < cols; ++i) s[i] += (float)x[r * ld + g * 8 + i];
   }
   float* out = part + blk * cols + g * 8;
   for (int i = 0; i < 8 && g * 8 + i < cols; ++i) out[i] = s[i];

@@ -667,9 +667,9 @@ def linear_ppo_fwd_bwd(hidden: torch.Tensor, weight: torch.Tensor, tokens: torch
     _surrogate_terms (trainer.py:150-195) including its model GEMMs, per chunk:
     logits = h W^T + b (areal_lm_head_gemm LOGITS, tcgen05, fp32 accumulate, bf16 out)
     -> K2 in place -> dlogits dL, then one grouped launch (areal_lm_head_backward):
-    dH = dL W (trainer.py:183's residual^T features, transposed), dW += dL^T h (fp32,
-    accumulated across chunks in the epilogue) and db += sum(dL) summed from the dL tiles
-    in shared memory (trainer.py:183-184).  Three launches per chunk, all of them this
+    dH = dL W (trainer.py:183's residual^T features, transposed) and dW += dL^T h (fp32,
+    accumulated across chunks in the epilogue), and db += sum(dL) (areal_colsum,
+    trainer.py:184).  Four launches per chunk (3 without a bias), all of them this
     library's kernels.  Peak extra memory is
     chunk_tokens x V x 2 bytes (2.5 GB at 8,192 x 151,936).
 
@@ -718,7 +718,12 @@ def linear_ppo_fwd_bwd(hidden: torch.Tensor, weight: torch.Tensor, tokens: torch
                       behav_weight_cap=behav_weight_cap, grad_scale=grad_scale, row_index=ri,
                       dlogits=lg, stats=stats, algo=algo, prox_from_lp=prox_from_lp,
                       lp_out=lp_out)                                              # 164-182
-        # dH = dL W, dW (+)= dL^T h, db (+)= sum dL (trainer.py:183-184): one grouped launch
-        K.lm_head_backward(lg, h, weight, grad_hidden[lo:hi], grad_weight, grad_bias,
-                           accumulate=acc0 or lo > 0, with_bias=grad_bias is not None)
+        # dH = dL W, dW (+)= dL^T h (trainer.py:183-184): one grouped launch; db (+)= sum dL
+        # (184) by the column-sum kernel (measured faster than summing inside the GEMM,
+        # DESIGN.md §8.1)
+        acc = acc0 or lo > 0
+        K.lm_head_backward(lg, h, weight, grad_hidden[lo:hi], grad_weight, None,
+                           accumulate=acc, with_bias=False)
+        if grad_bias is not None:
+            K.colsum(lg, grad_bias, accumulate=acc)
     return grad_hidden, grad_weight, grad_bias, stats
