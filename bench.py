@@ -509,6 +509,17 @@ def run_ours(args, cfg):
     k45_ms = sum(s.elapsed_time(e) for s, e in runner.k45_events)
     k2_bytes, k1_bytes = runner.k2_bytes, runner.k1_bytes
     n_k2 = len(runner.k2_events)
+    # K3 device time alone (the in-step events also hold the host's launch overhead of a
+    # sub-100 us kernel): 20 back-to-back launches on the step's rollouts
+    k3_s, k3_e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    runner.advantages(ro)
+    torch.cuda.synchronize()
+    k3_s.record()
+    for _ in range(20):
+        runner.advantages(ro)
+    k3_e.record()
+    torch.cuda.synchronize()
+    k3_kernel_us = 1e3 * k3_s.elapsed_time(k3_e) / 20
 
     # ---------------- e2e: public API with pinned host inputs and a D2H of the result
     e2e_steps = max(1, args.e2e_steps)
@@ -585,7 +596,9 @@ def run_ours(args, cfg):
                     bytes_per_token=V * es + 16, ms_per_step=k1_ms / args.steps),
             k2=dict(ms_per_step=k2_ms / args.steps, tokens_per_s=T / (k2_ms / args.steps * 1e-3)),
             k3=dict(kernel="areal_advantages (K3)", us_per_step=1e3 * k3_ms / args.steps,
-                    mode=hp.adv_mode, norm=hp.adv_norm),
+                    kernel_us=k3_kernel_us, mode=hp.adv_mode, norm=hp.adv_norm,
+                    note="us_per_step: in-step events incl. the host launch; kernel_us: "
+                         "back-to-back launches (one cooperative kernel in reference mode)"),
             k4_k5=dict(kernel="areal_plan_microbatches + areal_fill_gather (K4/K5)",
                        us_per_step=1e3 * k45_ms / args.steps,
                        note="all minibatches' allocation + packing plan, including the one "
