@@ -659,7 +659,12 @@ def main():
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     ap.add_argument("--share-gpu", action="store_true",
                     help="all ranks on cuda:0 (functional multi-rank check on one GPU)")
+    ap.add_argument("--lib", default=None,
+                    help="tuning only: a compile-time variant from tools/variants.py")
     args = ap.parse_args()
+    if args.lib:
+        from paper_2505_24298_b200 import _lib
+        _lib.use_library(args.lib)
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
     if args.config is None:

@@ -684,6 +684,7 @@ static size_t tmem_smem_bytes(int nslots) {
 template <typename T, bool ENT, bool UNAL = false>
 static int launch_tmem(PpoArgs a, cudaStream_t stream, const DevInfo& d, int nslots) {
   if (a.vocab >= (int64_t)1 << 30) return AREAL_ERR_UNSUPPORTED;  // 32-bit element indices
+  if (a.n_rows >= ((int64_t)1 << 31) - 4096) return AREAL_ERR_UNSUPPORTED;  // int row queue
   a.cluster_size = 1;
   a.slice16 = (a.vocab * (int64_t)sizeof(T)) / 16;
   a.nslots = nslots;

@@ -114,6 +114,10 @@ __device__ __forceinline__ uint32_t bf162_bits(__nv_bfloat162 v) {
   memcpy(&u, &v, 4);
   return u;
 }
+// Per-row timeline probe hook (tools/k2_timeline_probe.cu); empty in the product.
+#ifndef AREAL_K2_PROBE_TS
+#define AREAL_K2_PROBE_TS(ev, it) {}
+#endif
 constexpr int kTmemCols = 512;
 constexpr int kTmemMaxChunks = 14;    // TMEM + resident chunks: kTmemChunks + (nslots - 1)
 // Resident-tail cap (rows of <= 8 + kTResMax chunks stream nothing).  7 = every ring
@@ -143,13 +147,135 @@ __device__ __forceinline__ void st_out(V* p, V v, bool stream) {
   else *p = v;
 }
 
+// Dynamic row schedule: the producer takes each CTA's next row from a global counter
+// (first row = blockIdx.x) and publishes the row sequence through rowq / rowpub; the
+// math warps and the epilogue walk the same sequence.  With the static cid + k * grid
+// assignment the launch waited for its slowest CTA: CTA spans over one launch ranged
+// 2.87-3.01 ms around a 2.93 ms median (tools/k2_timeline_probe.cu); dynamic rows took
+// K2 bf16 32768 x 151,936 from 6.45 to 6.86 TB/s in a burst (profiles/r02_k2_dynamic_rows.md).  The producer runs at most nslots + 3 rows ahead of the
+// epilogue (one ring chunk per row at least), so kRowQ entries never wrap onto a live row.
+constexpr int kRowQ = 16;
+static_assert(kRowQ >= 7 + 3 + 1, "row queue shorter than the producer's lead");
+// The objective / ratio / entropy sums are accumulated as 128-bit fixed point (2^-64
+// units): integer addition is associative, so the statistics do not depend on which CTA
+// processed which rows (the row schedule is dynamic) and stay bit-reproducible.
+struct Fx128 {
+  unsigned long long lo;  // fraction, 2^-64 units
+  long long hi;           // integer part (two's complement with lo)
+  double nf;              // non-finite terms (inf / NaN), added as doubles
+};
+__device__ __forceinline__ void fx_add(Fx128& acc, unsigned long long lo, long long hi) {
+  const unsigned long long l = acc.lo + lo;
+  acc.hi += hi + (l < lo ? 1 : 0);
+  acc.lo = l;
+}
+__device__ __forceinline__ void fx_add(Fx128& acc, double x) {
+  if (!isfinite(x)) {
+    acc.nf += x;
+    return;
+  }
+  if (fabs(x) >= 0x1p62) {  // beyond the fixed-point range: keep it exact-order-free as inf
+    acc.nf += x > 0 ? INFINITY : -INFINITY;
+    return;
+  }
+  const double f = floor(x);
+  // x - f in [0, 1) is exact; scaled by 2^64 it is an exact double below 2^64
+  fx_add(acc, __double2ull_rz(ldexp(x - f, 64)), (long long)f);
+}
+__device__ __forceinline__ double fx_value(const Fx128& acc) {
+  return ((double)acc.hi + ldexp((double)acc.lo, -64)) + acc.nf;
+}
 struct TmemTail {
+  int rowq[kRowQ];                            // row sequence (producer -> consumers)
+  unsigned int rowpub;                        // rows published so far
   uint64_t bcbar[2];                          // epilogue -> math warps (row parity)
   float red[2][kTW][3];            // per-warp partials (row parity)
   RingBcast bc[2];
-  double st[AREAL_N_STATS];
-  float cw[2][kTmemMaxChunks][kTW];  // shift c of the stored e (row parity)
+  double st[AREAL_N_STATS];                   // counters (exact integers in double)
+  Fx128 fx[3];                                // objective, ratio, entropy sums
+  // shift c of the stored e (row parity): TMEM chunks, then up to kTResMax resident
+  // chunks (a streaming row's resident tail has kTResMax = 7 chunks: index 14)
+  float cw[2][kTmemChunks + kTResMax][kTW];
 };
+
+// k-th row of this CTA's sequence (-1: none left).  Published well before it is needed
+// (the producer announces row k+1 as soon as row k's last chunk is issued), so the
+// acquire load almost never spins.
+__device__ __forceinline__ int tmem_row(const TmemTail* tail, int k) {
+  unsigned int pub;
+  do {
+    asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(pub) : "r"(smem_u32(&tail->rowpub)) : "memory");
+  } while (pub <= (unsigned int)k);
+  return tail->rowq[k % kRowQ];
+}
+__device__ __forceinline__ void tmem_publish_row(TmemTail* tail, int k, int row) {
+  tail->rowq[k % kRowQ] = row;
+  asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_u32(&tail->rowpub)), "r"((unsigned int)(k + 1))
+               : "memory");
+}
+// stats_add with the three sums in fixed point (see Fx128)
+__device__ __forceinline__ void stats_add_fx(TmemTail* tail, const TokenTerms& t, double ent) {
+  double* st = tail->st;
+  fx_add(tail->fx[0], t.obj);
+  st[AREAL_STAT_N_VALID] += t.valid ? 1.0 : 0.0;
+  st[AREAL_STAT_N_CLIPPED] += t.clipped ? 1.0 : 0.0;
+  if (t.valid) fx_add(tail->fx[1], t.ratio);
+  st[AREAL_STAT_N_EXCLUDED] += t.valid ? 0.0 : 1.0;
+  st[AREAL_STAT_N_MASKED] += t.masked ? 1.0 : 0.0;
+  if (t.valid) fx_add(tail->fx[2], ent);
+  st[AREAL_STAT_N_TOKENS] += 1.0;
+}
+// Grid reduction of the TMEM kernel's statistics: every CTA writes its counters and
+// fixed-point sums to the workspace, the last CTA (atomic ticket) adds them up — integer
+// sums, so the result does not depend on the order — and re-arms the ticket and the
+// row counter.
+__device__ void finalize_stats_fx(const PpoArgs& a, const TmemTail* tail) {
+  __shared__ unsigned int s_last;
+  // per-CTA record: 8 doubles (counters) + 3 x (lo, hi, nf)
+  constexpr int kRec = AREAL_N_STATS + 9;
+  double* rec = a.partials + (size_t)blockIdx.x * kRec;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int j = 0; j < AREAL_N_STATS; ++j) rec[j] = tail->st[j];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      reinterpret_cast<unsigned long long*>(rec)[AREAL_N_STATS + 3 * j] = tail->fx[j].lo;
+      reinterpret_cast<long long*>(rec)[AREAL_N_STATS + 3 * j + 1] = tail->fx[j].hi;
+      rec[AREAL_N_STATS + 3 * j + 2] = tail->fx[j].nf;
+    }
+    __threadfence();
+    const unsigned int ticket = atomicAdd(a.counter, 1u);
+    s_last = (ticket == gridDim.x - 1) ? 1u : 0u;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (threadIdx.x < AREAL_N_STATS) {
+    const int j = threadIdx.x;
+    const volatile double* p = a.partials;
+    double v;
+    const int f = j == AREAL_STAT_OBJECTIVE_SUM ? 0 : j == AREAL_STAT_RATIO_SUM ? 1
+                : j == AREAL_STAT_ENTROPY_SUM ? 2 : -1;
+    if (f < 0) {
+      v = 0.0;  // counters: integer-valued doubles, exact in any order
+      for (unsigned int b = 0; b < gridDim.x; ++b) v += p[(size_t)b * kRec + j];
+    } else {
+      Fx128 acc{0ull, 0ll, 0.0};
+      const volatile unsigned long long* q = reinterpret_cast<const volatile unsigned long long*>(a.partials);
+      for (unsigned int b = 0; b < gridDim.x; ++b) {
+        const size_t o = (size_t)b * kRec + AREAL_N_STATS + 3 * f;
+        fx_add(acc, q[o], (long long)q[o + 1]);
+        acc.nf += p[o + 2];
+      }
+      v = fx_value(acc);
+    }
+    a.stats[j] += v;
+  }
+  if (threadIdx.x == 0) {
+    *a.counter = 0u;
+    a.counter[1] = 0u;  // dynamic row counter
+  }
+}
 
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
   asm volatile(
@@ -474,6 +600,8 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
     mbar_init(&tail->bcbar[0], 1);
     mbar_init(&tail->bcbar[1], 1);
     for (int j = 0; j < AREAL_N_STATS; ++j) tail->st[j] = 0.0;
+    for (int j = 0; j < 3; ++j) tail->fx[j] = Fx128{0ull, 0ll, 0.0};
+    tail->rowpub = 0u;
     fence_mbar_init_cluster();
   }
   if (warp == kTEpilogue) {  // one warp allocates (and later frees) all of TMEM
@@ -495,12 +623,18 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
       Cursor cur = {0u, 0u};
       uint32_t used = 0;
       const uint64_t pol_keep = l2_policy_evict_last(), pol_drop = l2_policy_evict_first();
-      for (int64_t row = cid; row < a.n_rows; row += ncl) {
+      int64_t row = cid;
+      for (int k = 0;; ++k) {
+        tmem_publish_row(tail, k, row < a.n_rows ? (int)row : -1);
+        if (row >= a.n_rows) break;
+        // the next row: claimed now, used after this row's loads are issued
+        const int64_t row_next = ncl + (int64_t)atomicAdd(a.counter + 1, 1u);
         const RowGeo geo = row_geo<T, UNAL>(a, row, nchunks);
         const char* src = geo.src(a, row);
         for (int c = 0; c < nchunks; ++c) {
           if (used >= nslots) mbar_wait(&empty[cur.slot], cur.phase ^ 1u);
           else ++used;
+          if (c == 0) AREAL_K2_PROBE_TS(7, k)
           const uint32_t bytes = (uint32_t)(c < nchunks - 1 ? kChunkBytes : geo.last_bytes);
           mbar_arrive_expect_tx(&full[cur.slot], bytes);
           if ((kL2Hints & 1) && S > 0)
@@ -511,12 +645,15 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
                      &full[cur.slot]);
           cur.next(nslots);
         }
+        row = row_next;
       }
     }
   } else if (warp == kTEpilogue) {
     // ================= epilogue: merge the 16 partials, fp64 per-token epilogue
-    int it = 0;
-    for (int64_t row = cid; row < a.n_rows; row += ncl, ++it) {
+    for (int it = 0;; ++it) {
+      const int row_i = tmem_row(tail, it);
+      if (row_i < 0) break;
+      const int64_t row = row_i;
       const int par = it & 1;
       int64_t idx = 0, tok = -1;
       double xa = 0.0, sc_behav = 0.0, sc_prox = 0.0, sc_adv = 0.0;
@@ -530,7 +667,9 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
         sc_adv = a.adv[idx];
         sc_ver = a.versions ? a.versions[idx] : 0;
       }
+      if (lane == 0) AREAL_K2_PROBE_TS(8, it)
       named_bar_sync(kBarPartials, kTBarThreads);
+      if (lane == 0) AREAL_K2_PROBE_TS(0, it)
       RowStat<A> w;
       if (lane < kTW) {
         w.m = tail->red[par][lane][0];
@@ -540,6 +679,7 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
         w.init();
       }
       RowStat<A> tot = warp_merge(w);
+      if (lane == 0) AREAL_K2_PROBE_TS(9, it)
       const bool slow = kFixedShift && !(tot.s < INFINITY);  // overflow (or NaN logits)
       if (slow) {
         const int hb = (int)((uintptr_t)(a.logits + row * a.ld_in_bytes) & 15);
@@ -561,9 +701,11 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
       const double e_scale = __shfl_sync(0xffffffffu, ex, 0);
       const double e_ratio = __shfl_sync(0xffffffffu, ex, 1);
       const double e_p = __shfl_sync(0xffffffffu, ex, 2);
+      if (lane == 0) AREAL_K2_PROBE_TS(10, it)
       if (lane == 0) {
         const TokenTerms t = ppo_token_terms(a.decoupled ? e_scale : 1.0, e_ratio, sc_adv, sc_ver, a);
         const double gc = a.grad_scale * t.coef;
+        AREAL_K2_PROBE_TS(11, it)
         RingBcast& b = tail->bc[par];
         b.gc = gc;
         b.lse = (double)lse_s;
@@ -571,7 +713,8 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
         b.dtok = to_bits<T>(Traits<T>::from_acc((A)(gc * (e_p - 1.0))));
         b.slow = slow ? 1 : 0;
         mbar_arrive(&tail->bcbar[par]);
-        stats_add(tail->st, t, ent);
+        AREAL_K2_PROBE_TS(1, it)
+        stats_add_fx(tail, t, ent);
         if (a.lp_out) a.lp_out[idx] = lp;
         if (ENT && a.ent_out) a.ent_out[idx] = ent;
       }
@@ -582,8 +725,10 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
     int la = 0;             // chunks of the current row folded by the previous lookahead
     RowStat<A> carry;
     carry.init();
-    int it = 0;
-    for (int64_t row = cid; row < a.n_rows; row += ncl, ++it) {
+    for (int it = 0;; ++it) {
+      const int row_i = tmem_row(tail, it);
+      if (row_i < 0) break;
+      const int64_t row = row_i;
       const int par = it & 1;
       float* cw = &tail->cw[par][0][0];  // [chunk][warp]
       const RowGeo geo = row_geo<T, UNAL>(a, row, nchunks);
@@ -630,15 +775,18 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
         tail->red[par][warp][1] = rs.s;
         tail->red[par][warp][2] = rs.sx;
       }
+      if (lane == 0 && warp == 0) AREAL_K2_PROBE_TS(2, it)
+      if (lane == 0 && warp == kTW - 1) AREAL_K2_PROBE_TS(3, it)
       named_bar_arrive(kBarPartials, kTBarThreads);
       // ---- lookahead: fold the next row's first chunks (e in place) during the epilogue
-      const bool has_next = row + ncl < a.n_rows;
+      const int row_nx = tmem_row(tail, it + 1);
+      const bool has_next = row_nx >= 0;
       const int la_next = has_next ? la_max : 0;
       float* cwn = &tail->cw[par ^ 1][0][0];
       RowStat<A> nxt;
       nxt.init();
       Cursor lc = after;
-      const RowGeo geo_n = (UNAL && has_next) ? row_geo<T, UNAL>(a, row + ncl, nchunks) : geo;
+      const RowGeo geo_n = (UNAL && has_next) ? row_geo<T, UNAL>(a, row_nx, nchunks) : geo;
       for (int c = 0; c < la_next; ++c) {
         mbar_wait(&full[lc.slot], lc.phase);
         const int nvec = nvec_of(c, geo_n);
@@ -653,7 +801,9 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
       carry = nxt;
       la = la_next;
 
+      if (lane == 0 && warp == 0) AREAL_K2_PROBE_TS(4, it)
       mbar_wait(&tail->bcbar[par], (it >> 1) & 1);
+      if (lane == 0 && warp == 0) AREAL_K2_PROBE_TS(5, it)
       const RingBcast b = tail->bc[par];
       const float g = (float)b.gc;
       const float lse_s = (float)b.lse;
@@ -781,6 +931,7 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
             reinterpret_cast<T*>(drow)[st] = dtok;
         }
       }
+      if (lane == 0 && warp == 0) AREAL_K2_PROBE_TS(6, it)
       cur = after;
     }
     tmem_fence_before();
@@ -791,9 +942,7 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(kTmemCols)
                  : "memory");
   }
-  double cta[AREAL_N_STATS];
-  for (int j = 0; j < AREAL_N_STATS; ++j) cta[j] = tail->st[j];
-  finalize_stats(a, cta, kTThreads);
+  finalize_stats_fx(a, tail);
 }
 
 }  // namespace areal

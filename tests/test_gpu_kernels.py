@@ -208,6 +208,47 @@ def test_ppo_stats_accumulate_and_deterministic():
     assert abs(float(s1[0] - s2[0])) < 1e-9
 
 
+@pytest.mark.parametrize("dt,V", [("bf16", 151936), ("bf16", 32000), ("f32", 151936)])
+def test_ppo_tmem_dynamic_rows_deterministic(dt, V):
+    """The TMEM K2 hands rows to CTAs dynamically (a global row counter) and sums the
+    objective / ratio / entropy in 128-bit fixed point: repeated launches give
+    bit-identical statistics, lp and dlogits; the ratio and entropy sums equal fp64 sums
+    of the kernel's own per-token outputs to 1e-12 relative, the counters and the
+    objective agree with the one-warp kernel (static fp64 reduction)."""
+    T = 2048 if V > 100000 else 6000
+    g = torch.Generator(device="cuda").manual_seed(11)
+    lg = (torch.randn(T, V, device="cuda", generator=g, dtype=torch.float32) * 2).to(DT[dt])
+    tok = torch.randint(0, V, (T,), device="cuda", generator=g)
+    lp, _ = K.logprob_fwd(lg, tok)
+    prox = lp + 0.05 * torch.randn(T, device="cuda", generator=g, dtype=torch.float64)
+    behav = prox + 0.2 * torch.randn(T, device="cuda", generator=g, dtype=torch.float64)
+    adv = torch.randn(T, device="cuda", generator=g, dtype=torch.float64)
+    outs = []
+    for _ in range(3):
+        lp_o = torch.zeros(T, dtype=torch.float64, device="cuda")
+        ent_o = torch.zeros(T, dtype=torch.float64, device="cuda")
+        dl, st = K.ppo_fwd_bwd(lg, tok, behav, prox, adv, lp_out=lp_o, entropy_out=ent_o)
+        outs.append((dl, st, lp_o, ent_o))
+    for dl, st, lp_o, ent_o in outs[1:]:
+        assert torch.equal(st, outs[0][1])
+        assert torch.equal(lp_o, outs[0][2]) and torch.equal(ent_o, outs[0][3])
+        assert torch.equal(dl, outs[0][0])
+    _, sw = K.ppo_fwd_bwd(lg, tok, behav, prox, adv, algo="warp",
+                          entropy_out=torch.zeros(T, dtype=torch.float64, device="cuda"))
+    s0, s1 = outs[0][1].cpu().numpy(), sw.cpu().numpy()
+    for j in (1, 4, 5, 7):  # counters: exact (n_clipped may differ at the clip boundary)
+        assert s0[j] == s1[j], (j, s0[j], s1[j])
+    assert abs(s0[2] - s1[2]) <= 2
+    lp_o, ent_o = outs[0][2], outs[0][3]
+    ratio = float(torch.exp(lp_o - prox).sum())
+    assert abs(s0[3] - ratio) <= 1e-12 * abs(ratio), (s0[3], ratio)
+    ent = float(ent_o.sum())
+    assert abs(s0[6] - ent) <= 1e-12 * abs(ent), (s0[6], ent)
+    # the two kernels' fp32 log-sum-exps differ by ~1e-7 relative, so each token's
+    # objective differs by ~1e-6 |adv|: bound the sum by T x that
+    assert abs(s0[0] - s1[0]) <= 1e-6 * T, (s0[0], s1[0])
+
+
 @pytest.mark.parametrize("algo", ["warp", "ring"])
 def test_ppo_matches_reference_golden(algo):
     for c in load_cases("surrogate.npz"):

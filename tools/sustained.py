@@ -1,12 +1,20 @@
 """Sustained (power-capped) bandwidth: torch copy vs K1 / K2 over ~4 s each, CUDA events.
 MEASURED_PEAKS.json's hbm_gbs is a best-of-10 burst; inside bench.py's ~2 s timed region
 the GPU runs at its power cap, so this is the like-for-like denominator.
-    python tools/sustained.py"""
-import json, os, sys
+    python tools/sustained.py [--lib build/variants/libareal_b200_X.so] [--which copy,k1,k2]"""
+import argparse, json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
-from paper_2505_24298_b200 import kernels as K
+from paper_2505_24298_b200 import _lib
+ap = argparse.ArgumentParser()
+ap.add_argument("--lib", default=None, help="a tuning build from tools/variants.py")
+ap.add_argument("--which", default="copy,k1,k2")
+ap.add_argument("--seconds", type=float, default=4.0)
+args = ap.parse_args()
+if args.lib:
+    _lib.use_library(args.lib)
+from paper_2505_24298_b200 import kernels as K  # noqa: E402
 
 dev = torch.device("cuda", 0)
 T, V = 32768, 151936
@@ -23,7 +31,8 @@ nbytes = x.numel() * 2
 from bench import ClockSampler  # noqa: E402
 
 
-def run(fn, seconds=4.0):
+def run(fn, seconds=None):
+    seconds = seconds or args.seconds
     fn(); torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record(); fn(); e.record(); torch.cuda.synchronize()
@@ -39,14 +48,21 @@ def run(fn, seconds=4.0):
     return s.elapsed_time(e) / n, n
 
 
-out = {}
-ms, n = run(lambda: y.copy_(x))
-out["copy"] = dict(ms=ms, iters=n, gbs=2 * nbytes / ms / 1e6, **run.last_clock)
-ms, n = run(lambda: K.logprob_fwd(x, tok, lp_out=lp, with_entropy=False))
-out["k1"] = dict(ms=ms, iters=n, gbs=T * (V * 2 + 16) / ms / 1e6, **run.last_clock)
-ms, n = run(lambda: K.ppo_fwd_bwd(x, tok, behav, lp, adv, dlogits=y, stats=stats))
-out["k2"] = dict(ms=ms, iters=n, gbs=T * (2 * V * 2 + 52) / ms / 1e6, **run.last_clock)
-ms, n = run(lambda: y.copy_(x))
-out["copy_again"] = dict(ms=ms, iters=n, gbs=2 * nbytes / ms / 1e6, **run.last_clock)
-out["k2_frac_of_sustained_copy"] = out["k2"]["gbs"] / max(out["copy"]["gbs"], out["copy_again"]["gbs"])
+out = {"lib": args.lib}
+which = args.which.split(",")
+if "copy" in which:
+    ms, n = run(lambda: y.copy_(x))
+    out["copy"] = dict(ms=ms, iters=n, gbs=2 * nbytes / ms / 1e6, **run.last_clock)
+if "k1" in which:
+    ms, n = run(lambda: K.logprob_fwd(x, tok, lp_out=lp, with_entropy=False))
+    out["k1"] = dict(ms=ms, iters=n, gbs=T * (V * 2 + 16) / ms / 1e6, **run.last_clock)
+if "k2" in which:
+    ms, n = run(lambda: K.ppo_fwd_bwd(x, tok, behav, lp, adv, dlogits=y, stats=stats))
+    out["k2"] = dict(ms=ms, iters=n, gbs=T * (2 * V * 2 + 52) / ms / 1e6, **run.last_clock)
+if "copy" in which:
+    ms, n = run(lambda: y.copy_(x))
+    out["copy_again"] = dict(ms=ms, iters=n, gbs=2 * nbytes / ms / 1e6, **run.last_clock)
+    if "k2" in which:
+        out["k2_frac_of_sustained_copy"] = out["k2"]["gbs"] / max(out["copy"]["gbs"],
+                                                                  out["copy_again"]["gbs"])
 print(json.dumps(out))
