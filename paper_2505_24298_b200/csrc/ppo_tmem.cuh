@@ -127,13 +127,6 @@ constexpr int kTmemMaxChunks = 14;    // TMEM + resident chunks: kTmemChunks + (
 #define AREAL_K2_RES_MAX 7
 #endif
 constexpr int kTResMax = AREAL_K2_RES_MAX;
-// Pass-2 chunk order: 0 = row order; 1 = resident tail, streamed, TMEM; 2 = resident
-// tail, TMEM, streamed.  Writing the resident tail first frees the producer's ring
-// slots early.
-#ifndef AREAL_K2_P2_ORDER
-#define AREAL_K2_P2_ORDER 0
-#endif
-constexpr int kP2Order = AREAL_K2_P2_ORDER;
 // L2 policy for rows with streamed chunks: bit 0 = TMA loads of streamed chunks
 // evict_last (the rest evict_first) so pass 2's re-read hits L2; bit 1 = dlogits
 // stores evict-first (st.global.cs) so they do not push those chunks out.
@@ -851,76 +844,77 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
           cs.next(nslots);
         }
       } else {
-      const bool st_stream = (kL2Hints & 2) && S > 0;
-      for (int k = 0; k < nchunks; ++k) {
-        // chunk order (kP2Order): row order by default; 1 / 2 put the resident tail
-        // first so its ring slots go back to the producer early (measured no better)
-        const int c = kP2Order == 0 ? k
-                      : k < R ? nchunks - R + k
-                      : kP2Order == 1 ? (k < R + S ? ntm + (k - R) : k - R - S)
-                                      : k - R;
-        const int nvec = nvec_of(c, geo);
-        const int e0 = c * per_chunk - geo.head<T>();
-        const bool full = UNAL ? region_valid<T>(warp, e0, V)
-                               : (warp + 1) * (kTWBytes / 16) <= nvec;  // this warp's region
-        uint32_t wv[kTWords];
-        if (c >= ntm && c < ntm + S) {  // streamed chunk: dlogits from the logits
-          stream_chunk_dlogits<T, UNAL>(a, row, geo, V, drow, c, nvec, warp, lane, g, lse_s);
-          continue;
-        }
-        if (c < ntm) {
-          tmem_ldw(tmem_addr(tbase, warp, c), wv);
-          tmem_wait_ld();
-        } else {  // resident tail chunk (its full barrier completed in pass 1)
-          const uint32_t slot = (cur.slot + (uint32_t)c) % nslots;
-          const uint4* q = reinterpret_cast<const uint4*>(ring + (size_t)slot * kChunkBytes);
-          if (full) lds_raw<true>(q, warp, lane, nvec, wv);
-          else lds_raw<false>(q, warp, lane, nvec, wv);
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&empty[slot]);
-        }
-        const float F = g * fast_exp2(cw[cwi(c) * kTW + warp] - lse_s);
-        const float2 F2 = make_float2(F, F);
-        uint4* dst = reinterpret_cast<uint4*>(drow + (size_t)c * kChunkBytes);
-        // bf16 logits: e is stored as bf16 pairs, so dlogit = e * F is one packed
-        // bf16x2 multiply per two logits (HMUL2.BF16; F rounded to bf16, <= 2^-8
-        // relative, inside the bf16 contract) instead of unpack + FMUL2 + repack.
-        constexpr bool kPackedMul = std::is_same<T, __nv_bfloat16>::value && kK2PackedBf16Mul;
-        const __nv_bfloat162 Fb = __float2bfloat162_rn(F);
-        auto put = [&](int j, uint4 o) {
-          const int vi = t_vec_index(warp, lane, j);
-          if (!UNAL || full) st_out(&dst[vi], o, st_stream);
-          else store_vec<T>(dst, vi, o, e0 + vi * E, V, st_stream);
-        };
-        auto scale_store = [&](int j) {
-          if constexpr (kPackedMul) {
-            uint4 o;
-            o.x = bf162_bits(__hmul2(bits_bf162(wv[4 * j + 0]), Fb));
-            o.y = bf162_bits(__hmul2(bits_bf162(wv[4 * j + 1]), Fb));
-            o.z = bf162_bits(__hmul2(bits_bf162(wv[4 * j + 2]), Fb));
-            o.w = bf162_bits(__hmul2(bits_bf162(wv[4 * j + 3]), Fb));
-            put(j, o);
-          } else {
-            float f[E];
-            EFmt<T>::V::unpack(make_uint4(wv[4 * j], wv[4 * j + 1], wv[4 * j + 2], wv[4 * j + 3]), f);
-#pragma unroll
-            for (int e = 0; e < E; e += 2) {
-              const float2 d = fmul2(make_float2(f[e], f[e + 1]), F2);
-              f[e] = d.x;
-              f[e + 1] = d.y;
-            }
-            put(j, Vec<T>::pack(f));
+      // dlogits stores: evict-first only on rows with streamed chunks (their re-read must
+      // stay in L2); the two store flavours are separate loops, not per-store predicates
+      auto pass2 = [&](auto stream_tag) {
+        constexpr bool ST = decltype(stream_tag)::value;
+        uint32_t rslot = (cur.slot + (uint32_t)(ntm + S)) % nslots;  // first resident chunk's slot
+        for (int c = 0; c < nchunks; ++c) {
+          const int nvec = nvec_of(c, geo);
+          const int e0 = c * per_chunk - geo.head<T>();
+          const bool full = UNAL ? region_valid<T>(warp, e0, V)
+                                 : (warp + 1) * (kTWBytes / 16) <= nvec;  // this warp's region
+          uint32_t wv[kTWords];
+          if (c >= ntm && c < ntm + S) {  // streamed chunk: dlogits from the logits
+            stream_chunk_dlogits<T, UNAL>(a, row, geo, V, drow, c, nvec, warp, lane, g, lse_s);
+            continue;
           }
-        };
-        if (full) {  // branch-free
+          if (c < ntm) {
+            tmem_ldw(tmem_addr(tbase, warp, c), wv);
+            tmem_wait_ld();
+          } else {  // resident tail chunk (its full barrier completed in pass 1)
+            const uint4* q = reinterpret_cast<const uint4*>(ring + (size_t)rslot * kChunkBytes);
+            if (full) lds_raw<true>(q, warp, lane, nvec, wv);
+            else lds_raw<false>(q, warp, lane, nvec, wv);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[rslot]);
+            if (++rslot == nslots) rslot = 0;
+          }
+          const float F = g * fast_exp2(cw[cwi(c) * kTW + warp] - lse_s);
+          const float2 F2 = make_float2(F, F);
+          uint4* dst = reinterpret_cast<uint4*>(drow + (size_t)c * kChunkBytes);
+          // bf16 logits: e is stored as bf16 pairs, so dlogit = e * F is one packed
+          // bf16x2 multiply per two logits (HMUL2.BF16; F rounded to bf16, <= 2^-8
+          // relative, inside the bf16 contract) instead of unpack + FMUL2 + repack.
+          constexpr bool kPackedMul = std::is_same<T, __nv_bfloat16>::value && kK2PackedBf16Mul;
+          const __nv_bfloat162 Fb = __float2bfloat162_rn(F);
+          auto put = [&](int j, uint4 o) {
+            const int vi = t_vec_index(warp, lane, j);
+            if (!UNAL || full) st_out(&dst[vi], o, ST);
+            else store_vec<T>(dst, vi, o, e0 + vi * E, V, ST);
+          };
+          auto scale_store = [&](int j) {
+            if constexpr (kPackedMul) {
+              uint4 o;
+              o.x = bf162_bits(__hmul2(bits_bf162(wv[4 * j + 0]), Fb));
+              o.y = bf162_bits(__hmul2(bits_bf162(wv[4 * j + 1]), Fb));
+              o.z = bf162_bits(__hmul2(bits_bf162(wv[4 * j + 2]), Fb));
+              o.w = bf162_bits(__hmul2(bits_bf162(wv[4 * j + 3]), Fb));
+              put(j, o);
+            } else {
+              float f[E];
+              EFmt<T>::V::unpack(make_uint4(wv[4 * j], wv[4 * j + 1], wv[4 * j + 2], wv[4 * j + 3]), f);
 #pragma unroll
-          for (int j = 0; j < kTV; ++j) scale_store(j);
-        } else {
+              for (int e = 0; e < E; e += 2) {
+                const float2 d = fmul2(make_float2(f[e], f[e + 1]), F2);
+                f[e] = d.x;
+                f[e + 1] = d.y;
+              }
+              put(j, Vec<T>::pack(f));
+            }
+          };
+          if (full) {  // branch-free
 #pragma unroll
-          for (int j = 0; j < kTV; ++j)
-            if (t_vec_index(warp, lane, j) < nvec) scale_store(j);
+            for (int j = 0; j < kTV; ++j) scale_store(j);
+          } else {
+#pragma unroll
+            for (int j = 0; j < kTV; ++j)
+              if (t_vec_index(warp, lane, j) < nvec) scale_store(j);
+          }
         }
-      }
+      };
+      if ((kL2Hints & 2) && S > 0) pass2(std::true_type{});
+      else pass2(std::false_type{});
       }  // fast path
       {  // the one-hot element: owner of vector vt of chunk ct (stream index st)
         if (b.tok >= 0 && b.tok < a.vocab) {
