@@ -34,17 +34,28 @@ constexpr int BM = 128;                      // rows per CTA (TMEM lanes); 256 p
 constexpr int BN = 256;                      // accumulator columns (N per MMA)
 constexpr int BK = 64;                       // k-slab (one 128-byte swizzle row of 16-bit)
 constexpr int UMMA_K = 16;
-#ifndef LMH_STAGES
-#define LMH_STAGES 7
+// Epilogue output through shared memory + TMA tensor stores (f32 += by TMA reduce-add in
+// L2): one 32-row x 128-byte box per epilogue warp.  The register -> global path it
+// replaces wrote 16 bytes per thread into 32 different rows per instruction: twice the L2
+// write sectors and 8x the write requests of cuBLAS's epilogue (ncu r02bk).
+#ifndef LMH_TMA_STORE
+#define LMH_TMA_STORE 1
 #endif
-constexpr int STAGES = LMH_STAGES;          // 7 x 32 KB: the most that fits beside the barriers
+constexpr bool kTmaStore = LMH_TMA_STORE != 0;
+#ifndef LMH_STAGES
+#define LMH_STAGES (LMH_TMA_STORE ? 6 : 7)
+#endif
+constexpr int STAGES = LMH_STAGES;          // x 32 KB: the most that fits beside the barriers
+                                             // (and the epilogue's staging boxes)
 constexpr int A_BYTES = BM * BK * 2;         // per CTA per stage
 constexpr int B_BYTES = (BN / 2) * BK * 2;   // per CTA per stage: half of B
 constexpr int STAGE = A_BYTES + B_BYTES;
 constexpr int MN_BLOCK = 64 * 128;           // one 64-element MN block of a 64-row K slab
-constexpr int SMEM = STAGES * STAGE + 1024;  // + run-time 1024-B alignment
 constexpr int EPI_SPLIT = 2;                 // epilogue warps per TMEM lane quarter
 constexpr int EPI_THREADS = 128 * EPI_SPLIT;
+constexpr int EPI_BOX = 32 * 128;            // one warp's staging box: 32 rows x 128 B
+constexpr int EPI_SMEM = kTmaStore ? (EPI_THREADS / 32) * EPI_BOX : 0;
+constexpr int SMEM = STAGES * STAGE + EPI_SMEM + 1024;  // + run-time 1024-B alignment
 constexpr int DB_WARPS = 4;                  // column-sum warps (grad_b fused into DWEIGHT)
 constexpr int DB_FIRST_WARP = 2 + EPI_THREADS / 32;
 // launch kinds: one problem of a fixed op, or the grouped backward (DHIDDEN + DWEIGHT)
@@ -176,6 +187,7 @@ template <int KIND, typename T>
 __global__ void __launch_bounds__(kind_threads(KIND), 1)
     lmh_gemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmB0,
                     const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmB1,
+                    const __grid_constant__ CUtensorMap tmC0, const __grid_constant__ CUtensorMap tmC1,
                     const Args a) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
@@ -273,11 +285,15 @@ __global__ void __launch_bounds__(kind_threads(KIND), 1)
     const int half = (warp - 2) >> 2;
     const uint32_t lane_base = tbase + ((uint32_t)(q * 32) << 16);
     const uint32_t tempty0 = mapa_shared(smem_u32(&tempty[0]), 0u);
+    unsigned char* stg = smem + (size_t)STAGES * STAGE + (size_t)(warp - 2) * EPI_BOX;  // 1024-B aligned
+    uint4* srow = reinterpret_cast<uint4*>(stg + lane * 128);
     uint32_t acc = 0, acc_phase = 0;
     for (int u = unit0; u < a.n_units; u += unit_step) {
       const Tile t = unit_tile(a, u);
       const Prob& p = (KIND == KIND_BWD && t.prob == 1) ? a.p[1] : a.p[0];
-      const int64_t row = (int64_t)t.mt * (2 * BM) + (int64_t)rank * BM + q * 32 + lane;
+      const CUtensorMap* tmC = (KIND == KIND_BWD && t.prob == 1) ? &tmC1 : &tmC0;
+      const int32_t row0 = t.mt * (2 * BM) + (int32_t)rank * BM + q * 32;
+      const int64_t row = (int64_t)row0 + lane;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t tcol = lane_base + acc * BN;
@@ -307,7 +323,44 @@ __global__ void __launch_bounds__(kind_threads(KIND), 1)
               if (c0 + i < p.N) x[i] += __ldg(p.bias + c0 + i);
           }
         }
-        if (row < p.M && c0 < p.N) {
+        if (kTmaStore) {
+          // swizzled staging (16-byte chunk j of row r at j ^ (r & 7): conflict-free, the
+          // layout the 128-byte-swizzle tensor map expects), then one box per warp; TMA
+          // clips rows >= M and columns >= N
+          if (p.f32_out) {
+            if (lane == 0) bulk_wait_read<0>();  // the previous box left the staging buffer
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              srow[j ^ (lane & 7)] = make_uint4(__float_as_uint(x[4 * j]), __float_as_uint(x[4 * j + 1]),
+                                                __float_as_uint(x[4 * j + 2]), __float_as_uint(x[4 * j + 3]));
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              if (p.accumulate) tma_reduce_add_2d(tmC, stg, (int32_t)c0, row0);
+              else tma_store_2d(tmC, stg, (int32_t)c0, row0);
+              bulk_commit();
+            }
+          } else {  // 16-bit: two 32-column chunks per 64-column box
+            if ((c & 1) == 0) {
+              if (lane == 0) bulk_wait_read<0>();
+              __syncwarp();
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              srow[((c & 1) * 4 + i) ^ (lane & 7)] =
+                  make_uint4(pack2<T>(x[8 * i], x[8 * i + 1]), pack2<T>(x[8 * i + 2], x[8 * i + 3]),
+                             pack2<T>(x[8 * i + 4], x[8 * i + 5]), pack2<T>(x[8 * i + 6], x[8 * i + 7]));
+            if (c & 1) {
+              fence_proxy_async_smem();
+              __syncwarp();
+              if (lane == 0) {
+                tma_store_2d(tmC, stg, (int32_t)(c0 - 32), row0);
+                bulk_commit();
+              }
+            }
+          }
+        } else if (row < p.M && c0 < p.N) {
           if (p.f32_out) {
             float* dst = static_cast<float*>(p.C) + row * p.ldc + c0;
             if (c0 + 32 <= p.N) {
@@ -349,6 +402,7 @@ __global__ void __launch_bounds__(kind_threads(KIND), 1)
       acc ^= 1u;
       if (acc == 0) acc_phase ^= 1u;
     }
+    if (kTmaStore && lane == 0) bulk_wait<0>();  // the last boxes are written before exit
   } else if (KIND == KIND_BWD) {
     // ================= column sums (grad_b = sum over tokens of dL, trainer.py:184) of the
     // DWEIGHT A tiles while they sit in shared memory: for the N-tile-0 unit of each M-tile,
@@ -462,7 +516,7 @@ namespace lmh {
 
 struct HostProb {
   Prob p;
-  CUtensorMap tmA, tmB;
+  CUtensorMap tmA, tmB, tmC;
 };
 
 // Validate one GEMM and build its problem descriptor + tensor maps.
@@ -500,6 +554,9 @@ static int make_prob(HostProb& h, int op, const void* A, int64_t lda, const void
       break;
   }
   if (!ok) return AREAL_ERR_CUDA;
+  if (f32_out ? !make_store_map(&h.tmC, C, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, N, ldc)
+              : !make_store_map(&h.tmC, C, dt, 2, M, N, ldc))
+    return AREAL_ERR_CUDA;
   Prob& p = h.p;
   p.M = M;
   p.N = N;
@@ -553,7 +610,8 @@ static int launch(int kind, HostProb* hp, int n, int dtype, int sms, cudaStream_
   }
   a.n_units = units;
   if (units == 0) return AREAL_OK;
-  void (*kern)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap, const Args) = nullptr;
+  void (*kern)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap,
+               const CUtensorMap, const Args) = nullptr;
   const bool bf = dtype == AREAL_BF16;
   switch (kind) {
     case AREAL_LMH_LOGITS: kern = bf ? lmh_gemm_kernel<AREAL_LMH_LOGITS, __nv_bfloat16> : lmh_gemm_kernel<AREAL_LMH_LOGITS, __half>; break;
@@ -578,7 +636,9 @@ static int launch(int kind, HostProb* hp, int n, int dtype, int sms, cudaStream_
   cfg.numAttrs = 1;
   const CUtensorMap& a1 = n > 1 ? hp[1].tmA : hp[0].tmA;
   const CUtensorMap& b1 = n > 1 ? hp[1].tmB : hp[0].tmB;
-  if (cudaLaunchKernelEx(&cfg, kern, hp[0].tmA, hp[0].tmB, a1, b1, a) != cudaSuccess) return AREAL_ERR_CUDA;
+  const CUtensorMap& c1 = n > 1 ? hp[1].tmC : hp[0].tmC;
+  if (cudaLaunchKernelEx(&cfg, kern, hp[0].tmA, hp[0].tmB, a1, b1, hp[0].tmC, c1, a) != cudaSuccess)
+    return AREAL_ERR_CUDA;
   AREAL_CUDA_CHECK_LAUNCH();
   return AREAL_OK;
 }

@@ -11,9 +11,10 @@
 import argparse, json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
-from paper_2505_24298_b200 import kernels as K
+from paper_2505_24298_b200 import _lib
 
 ap = argparse.ArgumentParser()
+ap.add_argument("--lib", default=None, help="a tuning build from tools/variants.py")
 ap.add_argument("--rows", type=int, default=16384)
 ap.add_argument("--vocab", type=int, default=151936)
 ap.add_argument("--dim", type=int, default=1536)
@@ -26,6 +27,9 @@ ap.add_argument("--repeat", type=int, default=1, help="run the --which list this
 ap.add_argument("--cool", type=float, default=0.0, help="idle seconds before each timed item "
                 "(sustained GEMM load heats the part and the clocks fall)")
 a = ap.parse_args()
+if a.lib:
+    _lib.use_library(a.lib)
+from paper_2505_24298_b200 import kernels as K  # noqa: E402
 for kv in a.tune:
     k_, v_ = kv.split("=")
     K.set_tuning(k_, int(v_))
