@@ -70,7 +70,7 @@ constexpr int MAX_PROBS = 2;
 // grouped GEMM (both read dL; the second's units fill the first's last wave).
 struct Prob {
   int64_t M, N, K;
-  int32_t n_mt, n_nt, group_m, ksteps, units, unit_base;
+  int32_t n_mt, n_nt, n_np, group_m, ksteps, units, unit_base;  // units: cluster units (mt, N-tile pair)
   void* C;
   int64_t ldc;
   const float* bias;  // LOGITS: + bias[n]
@@ -83,14 +83,15 @@ struct Args {
   int32_t n_probs, n_units;
 };
 
-// unit -> (problem, M-tile, N-tile): problems in order; inside one, M fastest within a
-// group of group_m M-tiles, then N, then groups (the pairs in flight share k-slabs in L2)
-struct Tile { int prob, mt, nt; };
+// cluster unit -> (problem, M-tile, N-tile pair): problems in order; inside one, M fastest
+// within a group of group_m M-tiles, then N-tile pairs, then groups (the clusters in
+// flight share their k-slabs in L2).  Pair p of the cluster takes N-tile 2 * np + p.
+struct Tile { int prob, mt, np; };
 __device__ __forceinline__ Tile unit_tile(const Args& a, int u) {
   const int pi = (a.n_probs > 1 && u >= a.p[1].unit_base) ? 1 : 0;
-  const Prob& p = a.p[pi];
+  const Prob& p = pi ? a.p[1] : a.p[0];
   u -= p.unit_base;
-  const int per_group = p.group_m * p.n_nt;
+  const int per_group = p.group_m * p.n_np;
   const int full = p.n_mt / p.group_m;
   const int g = u / per_group;
   if (g < full) {
@@ -101,8 +102,8 @@ __device__ __forceinline__ Tile unit_tile(const Args& a, int u) {
   const int r = u - full * per_group;
   return Tile{pi, full * p.group_m + r % gm, r / gm};
 }
-__device__ __forceinline__ bool db_unit(const Args& a, const Tile& t) {
-  return a.p[t.prob].colsum != nullptr && t.nt == 0;
+__device__ __forceinline__ bool db_unit(const Args& a, const Tile& t, uint32_t pair) {
+  return (t.prob ? a.p[1] : a.p[0]).colsum != nullptr && t.np == 0 && pair == 0;
 }
 
 template <typename T> __device__ __forceinline__ uint32_t pack2(float x, float y);
@@ -122,13 +123,19 @@ template <> __device__ __forceinline__ float2 unpack2<__half>(uint32_t v) {
   return __half22float2(*reinterpret_cast<const __half2*>(&v));
 }
 
-// TMA loads of one unit's k-slabs (both CTAs; completion counted on the leader's barrier).
-// A_MN / B_MN: operand stored [K rows x MN cols] -> two 64-column boxes per CTA half.
-template <bool A_MN, bool B_MN>
+// TMA loads of one unit's k-slabs.  Cluster of 4 = 2 CTA pairs on one M-tile and two
+// N-tiles: each CTA loads its half of its pair's B, and a quarter of the pairs' common A
+// (its 128 A rows / columns split 64 + 64 between the two pairs) multicast to the CTA of
+// the same pair rank in both pairs; bytes are counted on each pair's leader barrier.
+// A_MN / B_MN: operand stored [K rows x MN cols] (64-column boxes).
+template <bool A_MN, bool B_MN, int CL>
 __device__ __forceinline__ void produce_unit(const CUtensorMap* mA, const CUtensorMap* mB, unsigned char* smem,
                                              uint64_t* full, uint64_t* empty, uint64_t* dbdone, int32_t m0,
-                                             int32_t n0, int ksteps, bool db, uint32_t rank, uint32_t& stage,
-                                             uint32_t& phase, uint32_t& db_pending, uint32_t& db_phase) {
+                                             int32_t n0, int ksteps, bool db, uint32_t r, uint32_t pair,
+                                             uint32_t& stage, uint32_t& phase, uint32_t& db_pending,
+                                             uint32_t& db_phase) {
+  const uint16_t a_mask = (uint16_t)((1u << r) | (1u << (2 + r)));
+  const int32_t ma = m0 + (int32_t)pair * 64;  // this CTA's 64 of the pair rank's 128 A rows / columns
   for (int ks = 0; ks < ksteps; ++ks) {
     mbar_wait(&empty[stage], phase ^ 1u);
     if (db_pending >> stage & 1u) {  // the column-sum warps still read this stage
@@ -138,27 +145,34 @@ __device__ __forceinline__ void produce_unit(const CUtensorMap* mA, const CUtens
     }
     if (db) db_pending |= 1u << stage;
     unsigned char* st = smem + (size_t)stage * STAGE;
-    const uint32_t bar0 = mapa_shared(smem_u32(&full[stage]), 0u);
-    if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * STAGE);
+    const uint32_t bar_lead = mapa_shared(smem_u32(&full[stage]), 2u * pair);  // own pair's leader
+    const uint32_t bar_any = mapa_shared(smem_u32(&full[stage]), 0u);           // even CTA of each pair
+    if (r == 0) mbar_arrive_expect_tx(&full[stage], 2 * STAGE);
     const int32_t k0 = ks * BK;
-    if (A_MN) {
-      tma_load_2d_cg2(mA, st, bar0, m0, k0);
-      tma_load_2d_cg2(mA, st + MN_BLOCK, bar0, m0 + 64, k0);
-    } else {
-      tma_load_2d_cg2(mA, st, bar0, k0, m0);
+    if (CL == 4) {
+      if (A_MN) tma_load_2d_cg2_mc(mA, st + pair * MN_BLOCK, bar_any, ma, k0, a_mask);
+      else tma_load_2d_cg2_mc(mA, st + pair * (A_BYTES / 2), bar_any, k0, ma, a_mask);
+    } else {  // CTA pair only: this CTA's 128 A rows / columns as two 64-wide boxes
+      if (A_MN) {
+        tma_load_2d_cg2(mA, st, bar_lead, m0, k0);
+        tma_load_2d_cg2(mA, st + MN_BLOCK, bar_lead, m0 + 64, k0);
+      } else {
+        tma_load_2d_cg2(mA, st, bar_lead, k0, m0);
+        tma_load_2d_cg2(mA, st + A_BYTES / 2, bar_lead, k0, m0 + 64);
+      }
     }
     if (B_MN) {
-      tma_load_2d_cg2(mB, st + A_BYTES, bar0, n0, k0);
-      tma_load_2d_cg2(mB, st + A_BYTES + MN_BLOCK, bar0, n0 + 64, k0);
+      tma_load_2d_cg2(mB, st + A_BYTES, bar_lead, n0, k0);
+      tma_load_2d_cg2(mB, st + A_BYTES + MN_BLOCK, bar_lead, n0 + 64, k0);
     } else {
-      tma_load_2d_cg2(mB, st + A_BYTES, bar0, k0, n0);
+      tma_load_2d_cg2(mB, st + A_BYTES, bar_lead, k0, n0);
     }
     if (++stage == STAGES) stage = 0, phase ^= 1u;
   }
 }
 
 // The unit's MMAs into one TMEM accumulator (leader CTA, one thread).
-template <bool A_MN, bool B_MN>
+template <bool A_MN, bool B_MN, int CL>
 __device__ __forceinline__ void mma_unit(unsigned char* smem, uint64_t* full, uint64_t* empty, uint64_t* landed,
                                          uint32_t landed_peer, uint32_t d_tmem, uint32_t idesc, int ksteps,
                                          bool db, uint32_t& stage, uint32_t& phase) {
@@ -178,12 +192,13 @@ __device__ __forceinline__ void mma_unit(unsigned char* smem, uint64_t* full, ui
     for (int kk = 0; kk < BK / UMMA_K; ++kk)
       mma_bf16_cg2(d_tmem, adesc + (uint64_t)(kk * a_step), bdesc + (uint64_t)(kk * b_step), idesc,
                    (ks | kk) != 0);
-    mma_commit_cg2(&empty[stage]);  // frees the stage in both CTAs once read
+    // frees the stage once read: in all four CTAs (the other pair's A quarters live here too)
+    mma_commit_cg2_mask(&empty[stage], CL == 4 ? 0xF : 0x3);
     if (++stage == STAGES) stage = 0, phase ^= 1u;
   }
 }
 
-template <int KIND, typename T>
+template <int KIND, typename T, int CL>
 __global__ void __launch_bounds__(kind_threads(KIND), 1)
     lmh_gemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmB0,
                     const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmB1,
@@ -196,13 +211,16 @@ __global__ void __launch_bounds__(kind_threads(KIND), 1)
   __shared__ uint32_t s_tbase;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_ctarank();
+  const uint32_t crank = cluster_ctarank();   // 0..CL-1
+  const uint32_t rank = crank & 1u;           // rank in the CTA pair (1 = the MMA peer)
+  const uint32_t pair = crank >> 1;           // which pair of the cluster (its N-tile)
+  constexpr int NPU = CL / 2;                 // N-tiles per unit (one per pair)
   const int unit0 = (int)cluster_id_x();
   const int unit_step = (int)nclusters_x();
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], CL / 2);  // one MMA commit from each pair
       mbar_init(&landed[s], 1);
       mbar_init(&dbdone[s], DB_WARPS);
     }
@@ -237,44 +255,46 @@ __global__ void __launch_bounds__(kind_threads(KIND), 1)
         const Tile t = unit_tile(a, u);
         const bool second = KIND == KIND_BWD && t.prob == 1;
         const int ksteps = second ? a.p[1].ksteps : a.p[0].ksteps;
-        const bool db = KIND == KIND_BWD && second && t.nt == 0 && a.p[1].colsum != nullptr;
+        // both pairs: pair 0's column-sum warps also read the A quarters pair 1 multicasts
+        // into pair 0, so pair 1's producer waits for them too
+        const bool db = KIND == KIND_BWD && second && db_unit(a, t, 0u);
         const int32_t m0 = t.mt * (2 * BM) + (int32_t)rank * BM;
-        const int32_t n0 = t.nt * BN + (int32_t)rank * (BN / 2);
+        const int32_t n0 = (NPU * t.np + (int32_t)pair) * BN + (int32_t)rank * (BN / 2);
         if (KIND == AREAL_LMH_LOGITS)
-          produce_unit<false, false>(&tmA0, &tmB0, smem, full, empty, dbdone, m0, n0, ksteps, false, rank, stage,
-                                     phase, db_pending, db_phase);
+          produce_unit<false, false, CL>(&tmA0, &tmB0, smem, full, empty, dbdone, m0, n0, ksteps, false, rank, pair,
+                                     stage, phase, db_pending, db_phase);
         else if (KIND == AREAL_LMH_DHIDDEN || (KIND == KIND_BWD && !second))
-          produce_unit<false, true>(&tmA0, &tmB0, smem, full, empty, dbdone, m0, n0, ksteps, false, rank, stage,
-                                    phase, db_pending, db_phase);
+          produce_unit<false, true, CL>(&tmA0, &tmB0, smem, full, empty, dbdone, m0, n0, ksteps, false, rank, pair,
+                                    stage, phase, db_pending, db_phase);
         else if (KIND == AREAL_LMH_DWEIGHT)
-          produce_unit<true, true>(&tmA0, &tmB0, smem, full, empty, dbdone, m0, n0, ksteps, false, rank, stage,
-                                   phase, db_pending, db_phase);
+          produce_unit<true, true, CL>(&tmA0, &tmB0, smem, full, empty, dbdone, m0, n0, ksteps, false, rank, pair,
+                                   stage, phase, db_pending, db_phase);
         else
-          produce_unit<true, true>(&tmA1, &tmB1, smem, full, empty, dbdone, m0, n0, ksteps, db, rank, stage,
-                                   phase, db_pending, db_phase);
+          produce_unit<true, true, CL>(&tmA1, &tmB1, smem, full, empty, dbdone, m0, n0, ksteps, db, rank, pair,
+                                   stage, phase, db_pending, db_phase);
       }
     }
   } else if (warp == 1) {
     // ================= MMA issuer (leader CTA)
     if (lane == 0 && rank == 0) {
       uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
-      const uint32_t landed_peer = mapa_shared(smem_u32(&landed[0]), 1u);
+      const uint32_t landed_peer = mapa_shared(smem_u32(&landed[0]), crank + 1u);
       for (int u = unit0; u < a.n_units; u += unit_step) {
         const Tile t = unit_tile(a, u);
         const bool second = KIND == KIND_BWD && t.prob == 1;
         const int ksteps = second ? a.p[1].ksteps : a.p[0].ksteps;
         const uint32_t idesc = second ? a.p[1].idesc : a.p[0].idesc;
-        const bool db = KIND == KIND_BWD && second && t.nt == 0 && a.p[1].colsum != nullptr;
+        const bool db = KIND == KIND_BWD && second && db_unit(a, t, pair);
         mbar_wait_cluster(&tempty[acc], acc_phase ^ 1u);
         tc_fence_after();
         const uint32_t d_tmem = tbase + acc * BN;
         if (KIND == AREAL_LMH_LOGITS)
-          mma_unit<false, false>(smem, full, empty, landed, landed_peer, d_tmem, idesc, ksteps, false, stage, phase);
+          mma_unit<false, false, CL>(smem, full, empty, landed, landed_peer, d_tmem, idesc, ksteps, false, stage, phase);
         else if (KIND == AREAL_LMH_DHIDDEN || (KIND == KIND_BWD && !second))
-          mma_unit<false, true>(smem, full, empty, landed, landed_peer, d_tmem, idesc, ksteps, false, stage, phase);
+          mma_unit<false, true, CL>(smem, full, empty, landed, landed_peer, d_tmem, idesc, ksteps, false, stage, phase);
         else
-          mma_unit<true, true>(smem, full, empty, landed, landed_peer, d_tmem, idesc, ksteps, db, stage, phase);
-        mma_commit_cg2(&tfull[acc]);  // accumulator complete -> epilogues of both CTAs
+          mma_unit<true, true, CL>(smem, full, empty, landed, landed_peer, d_tmem, idesc, ksteps, db, stage, phase);
+        mma_commit_cg2_mask(&tfull[acc], (uint16_t)(3u << (2 * pair)));  // -> epilogues of this pair
         acc ^= 1u;
         if (acc == 0) acc_phase ^= 1u;
       }
@@ -284,7 +304,7 @@ __global__ void __launch_bounds__(kind_threads(KIND), 1)
     const int q = warp & 3;
     const int half = (warp - 2) >> 2;
     const uint32_t lane_base = tbase + ((uint32_t)(q * 32) << 16);
-    const uint32_t tempty0 = mapa_shared(smem_u32(&tempty[0]), 0u);
+    const uint32_t tempty0 = mapa_shared(smem_u32(&tempty[0]), 2u * pair);  // this pair's MMA issuer
     unsigned char* stg = smem + (size_t)STAGES * STAGE + (size_t)(warp - 2) * EPI_BOX;  // 1024-B aligned
     uint4* srow = reinterpret_cast<uint4*>(stg + lane * 128);
     uint32_t acc = 0, acc_phase = 0;
@@ -305,7 +325,7 @@ __global__ void __launch_bounds__(kind_threads(KIND), 1)
         tmem_ld_wait();
         if (c + 1 < CH_PER_WARP) tmem_ld32_issue(tcol + (ch0 + c + 1) * 32, v[(c + 1) & 1]);
         float* x = v[c & 1];
-        const int64_t c0 = (int64_t)t.nt * BN + (ch0 + c) * 32;
+        const int64_t c0 = (int64_t)(NPU * t.np + (int)pair) * BN + (ch0 + c) * 32;
         if (p.bias != nullptr) {
           if (c0 + 32 <= p.N) {
             const float4* b4 = reinterpret_cast<const float4*>(p.bias + c0);
@@ -416,7 +436,7 @@ __global__ void __launch_bounds__(kind_threads(KIND), 1)
     for (int u = unit0; u < a.n_units; u += unit_step) {
       const Tile tl = unit_tile(a, u);
       const Prob& p = tl.prob == 1 ? a.p[1] : a.p[0];
-      if (!db_unit(a, tl)) {  // keep the stage counter in step with the pipeline
+      if (!db_unit(a, tl, pair)) {  // keep the stage counter in step with the pipeline
         stage = (uint32_t)((stage + p.ksteps) % STAGES);
         continue;
       }
@@ -434,7 +454,10 @@ __global__ void __launch_bounds__(kind_threads(KIND), 1)
           sum[4] += e2.x, sum[5] += e2.y, sum[6] += e3.x, sum[7] += e3.y;
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&dbdone[stage]);
+        if (lane == 0) {  // release the stage to this CTA's producer and to the other pair's
+          mbar_arrive(&dbdone[stage]);  // same-rank CTA, whose multicast writes here too
+          if (CL == 4) mbar_remote_arrive(mapa_shared(smem_u32(&dbdone[stage]), crank + 2u));
+        }
         if (++stage == STAGES) stage = 0;
       }
 #pragma unroll
@@ -519,6 +542,15 @@ struct HostProb {
   CUtensorMap tmA, tmB, tmC;
 };
 
+// Cluster shape per op: LOGITS (K = d, a short main loop) runs on plain CTA pairs; the
+// backward GEMMs (K = V or T) on 2 pairs sharing A through TMA multicast, which halves their
+// shared operand's L2 reads (ncu r02bk: cuBLAS reads half our L2 sectors) and took DWEIGHT
+// from 14.4-15.0 to 12.3-13.1 ms at 32,768 x 151,936 x 1,536 (profiles/r02_lmh_multicast.md).
+static int lmh_cluster(int op) { return op == AREAL_LMH_LOGITS ? 2 : 4; }
+// Clusters in flight, for the raster grouping only: 4-CTA clusters fill 33 of the 37
+// possible on a 148-SM B200 (GPC granularity; the launch itself queries the occupancy).
+static int max_clusters_hint(int sms, int cl) { return cl == 4 ? std::max(1, (sms * 9) / 40) : std::max(1, sms / 2); }
+
 // Validate one GEMM and build its problem descriptor + tensor maps.
 static int make_prob(HostProb& h, int op, const void* A, int64_t lda, const void* B, int64_t ldb, void* C,
                      int64_t ldc, int64_t M, int64_t N, int64_t K, const float* bias, float* colsum,
@@ -542,11 +574,11 @@ static int make_prob(HostProb& h, int op, const void* A, int64_t lda, const void
   switch (op) {
     case AREAL_LMH_LOGITS:  // A = H [M, K], B = W [N, K]
       if (lda < K || ldb < K) return AREAL_ERR_BAD_SHAPE;
-      ok = make_map(&h.tmA, A, dt, M, K, lda, BM) && make_map(&h.tmB, B, dt, N, K, ldb, BN / 2);
+      ok = make_map(&h.tmA, A, dt, M, K, lda, BM / 2) && make_map(&h.tmB, B, dt, N, K, ldb, BN / 2);
       break;
     case AREAL_LMH_DHIDDEN:  // A = dL [M, K], B = W [K, N]
       if (lda < K || ldb < N) return AREAL_ERR_BAD_SHAPE;
-      ok = make_map(&h.tmA, A, dt, M, K, lda, BM) && make_map(&h.tmB, B, dt, K, N, ldb, BK);
+      ok = make_map(&h.tmA, A, dt, M, K, lda, BM / 2) && make_map(&h.tmB, B, dt, K, N, ldb, BK);
       break;
     default:  // DWEIGHT: A = dL [K, M], B = H [K, N]
       if (lda < M || ldb < N) return AREAL_ERR_BAD_SHAPE;
@@ -563,7 +595,9 @@ static int make_prob(HostProb& h, int op, const void* A, int64_t lda, const void
   p.K = K;
   p.n_mt = (int32_t)((M + 2 * BM - 1) / (2 * BM));
   p.n_nt = (int32_t)((N + BN - 1) / BN);
-  p.units = p.n_mt * p.n_nt;
+  const int cl = lmh_cluster(op);
+  p.n_np = (p.n_nt + cl / 2 - 1) / (cl / 2);  // an odd last N-tile runs against zero-filled B, clipped
+  p.units = p.n_mt * p.n_np;
   p.unit_base = 0;
   p.ksteps = (int32_t)((K + BK - 1) / BK);
   p.C = C;
@@ -577,10 +611,10 @@ static int make_prob(HostProb& h, int op, const void* A, int64_t lda, const void
   // pairs in flight cover group_m M-tiles x (pairs / group_m) N-tiles: their A and B
   // k-slabs are shared through L2 (LOGITS: W read n_mt / 16 times, H once).  DWEIGHT's B
   // (H, T x d) stays in L2 whatever the order, while its A (dL) is the big stream: with
-  // group_m = 1 the pairs sharing an A tile have consecutive cluster ids (co-scheduled),
-  // which cut DRAM reads from 7.7 to 5.3 GB at T = 8,192 (ncu, profiles/r02_lmh_group_m.txt)
-  const int clusters = std::max(1, sms / 2);
-  p.group_m = p.n_nt >= clusters ? std::min(16, p.n_mt) : std::max(1, std::min(p.n_mt, clusters / p.n_nt));
+  // group_m = 1 the clusters sharing an A tile have consecutive ids (co-scheduled), which
+  // cut DRAM reads from 7.7 to 5.3 GB at T = 8,192 (ncu, profiles/r02_lmh_group_m.txt)
+  const int clusters = max_clusters_hint(sms, cl);
+  p.group_m = p.n_np >= clusters ? std::min(16, p.n_mt) : std::max(1, std::min(p.n_mt, clusters / p.n_np));
   if (op == AREAL_LMH_DWEIGHT) p.group_m = 1;
   if (tuning(AREAL_TUNE_LMH_GROUP_M) > 0) p.group_m = (int32_t)std::min<int64_t>(p.n_mt, tuning(AREAL_TUNE_LMH_GROUP_M));
   const uint32_t ab = dtype == AREAL_BF16 ? 1u : 0u;
@@ -613,27 +647,38 @@ static int launch(int kind, HostProb* hp, int n, int dtype, int sms, cudaStream_
   void (*kern)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap,
                const CUtensorMap, const Args) = nullptr;
   const bool bf = dtype == AREAL_BF16;
+  const int cl = lmh_cluster(kind == KIND_BWD ? AREAL_LMH_DWEIGHT : kind);
   switch (kind) {
-    case AREAL_LMH_LOGITS: kern = bf ? lmh_gemm_kernel<AREAL_LMH_LOGITS, __nv_bfloat16> : lmh_gemm_kernel<AREAL_LMH_LOGITS, __half>; break;
-    case AREAL_LMH_DHIDDEN: kern = bf ? lmh_gemm_kernel<AREAL_LMH_DHIDDEN, __nv_bfloat16> : lmh_gemm_kernel<AREAL_LMH_DHIDDEN, __half>; break;
-    case AREAL_LMH_DWEIGHT: kern = bf ? lmh_gemm_kernel<AREAL_LMH_DWEIGHT, __nv_bfloat16> : lmh_gemm_kernel<AREAL_LMH_DWEIGHT, __half>; break;
-    default: kern = bf ? lmh_gemm_kernel<KIND_BWD, __nv_bfloat16> : lmh_gemm_kernel<KIND_BWD, __half>; break;
+    case AREAL_LMH_LOGITS: kern = bf ? lmh_gemm_kernel<AREAL_LMH_LOGITS, __nv_bfloat16, 2> : lmh_gemm_kernel<AREAL_LMH_LOGITS, __half, 2>; break;
+    case AREAL_LMH_DHIDDEN: kern = bf ? lmh_gemm_kernel<AREAL_LMH_DHIDDEN, __nv_bfloat16, 4> : lmh_gemm_kernel<AREAL_LMH_DHIDDEN, __half, 4>; break;
+    case AREAL_LMH_DWEIGHT: kern = bf ? lmh_gemm_kernel<AREAL_LMH_DWEIGHT, __nv_bfloat16, 4> : lmh_gemm_kernel<AREAL_LMH_DWEIGHT, __half, 4>; break;
+    default: kern = bf ? lmh_gemm_kernel<KIND_BWD, __nv_bfloat16, 4> : lmh_gemm_kernel<KIND_BWD, __half, 4>; break;
   }
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM) != cudaSuccess)
     return AREAL_ERR_CUDA;
-  const int clusters = std::max(1, std::min(sms / 2, units));
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(2 * clusters);
+  cfg.gridDim = dim3(cl);
   cfg.blockDim = dim3(kind == KIND_BWD ? kind_threads(KIND_BWD) : kind_threads(0));
   cfg.dynamicSmemBytes = SMEM;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.x = cl;  // a CTA pair, or two pairs sharing A through multicast
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  // a persistent grid must be co-resident: 4-CTA clusters with this shared memory fit 33
+  // at a time on 148 SMs (GPC granularity), not 148 / 4 (the first multicast attempt
+  // launched 37 and ran its last clusters after the others: 47% tensor-pipe busy)
+  static int max_active[2][4] = {{0}};
+  int& ma = max_active[bf ? 1 : 0][kind & 3];
+  if (ma == 0 && (cudaOccupancyMaxActiveClusters(&ma, kern, &cfg) != cudaSuccess || ma < 1)) {
+    cudaGetLastError();
+    ma = 1;
+  }
+  const int clusters = std::max(1, std::min(ma, units));
+  cfg.gridDim = dim3(cl * clusters);
   const CUtensorMap& a1 = n > 1 ? hp[1].tmA : hp[0].tmA;
   const CUtensorMap& b1 = n > 1 ? hp[1].tmB : hp[0].tmB;
   const CUtensorMap& c1 = n > 1 ? hp[1].tmC : hp[0].tmC;

@@ -130,6 +130,25 @@ __device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, const 
                "r"(smem_u32(smem_src)), "r"(x), "r"(y)
                : "memory");
 }
+// Pair-mode TMA load multicast to the CTAs in `mask` (same smem offset in each); the
+// transaction bytes are counted on the barrier at `bar_cluster`'s offset in the even
+// (MMA-issuing) CTA of each destination pair (CUTLASS SM100_TMA_2SM_LOAD_MULTICAST).
+__device__ __forceinline__ void tma_load_2d_cg2_mc(const CUtensorMap* map, void* smem_dst, uint32_t bar_cluster,
+                                                   int32_t x, int32_t y, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(x), "r"(y), "h"(mask)
+      : "memory");
+}
+// commit to the barrier at the same offset in every CTA of `mask`
+__device__ __forceinline__ void mma_commit_cg2_mask(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
 
 static inline PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
