@@ -336,6 +336,8 @@ class DecoupledPPOStep:
         self.k1_bytes = 0
         self.k7_flops = 0
         self.record_events = False
+        self._ev_pool: list = []  # reused timing events (no event creation per launch)
+        self._ev_next = 0
         self._readback = None  # pinned buffer for the plan's host read
         self.h2d_bytes = 0     # host->device bytes of the last run() from HostRollouts
         self.last_plan = None
@@ -446,10 +448,23 @@ class DecoupledPPOStep:
                 ranges.append((lo, hi))
         return ranges
 
+    def reset_events(self) -> None:
+        """Start a timed region: clear the per-kernel event lists; the pooled events are
+        reused (read every elapsed_time of the previous region first)."""
+        self.k1_events, self.k2_events, self.k3_events, self.k45_events = [], [], [], []
+        self._ev_next = 0
+
+    def _event(self):
+        if self._ev_next == len(self._ev_pool):
+            self._ev_pool.append(torch.cuda.Event(enable_timing=True))
+        ev = self._ev_pool[self._ev_next]
+        self._ev_next += 1
+        return ev
+
     def _timed(self, events, fn):
         if not self.record_events:
             return fn()
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s, e = self._event(), self._event()
         s.record()
         out = fn()
         e.record()
