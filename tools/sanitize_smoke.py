@@ -1,4 +1,4 @@
-"""Small invocation of every kernel (K1-K7), for compute-sanitizer runs:
+"""Small invocation of every kernel (K1-K8), for compute-sanitizer runs:
     compute-sanitizer --tool memcheck python tools/sanitize_smoke.py"""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -42,5 +42,19 @@ for cg in (1, 2):
     w = torch.randn(5000, 256, device=dev, generator=g).to(torch.bfloat16)
     tok = torch.randint(0, 5000, (300,), device=dev, generator=g)
     K.linear_logprob_fwd(h, w, tok, bias=torch.randn(5000, device=dev), with_entropy=True, cta_group=cg)
+# LM-head GEMMs (K8): CTA-pair LOGITS, 2x2-cluster multicast DHIDDEN / DWEIGHT (+= through
+# TMA reduce-add) and the grouped backward with the fused column sum
+T, V, d = 600, 3000, 192
+h = torch.randn(T, d, device=dev, generator=g).to(torch.bfloat16)
+w = (torch.randn(V, d, device=dev, generator=g) / d ** 0.5).to(torch.bfloat16)
+ldv = (V + 7) // 8 * 8
+lg = torch.empty(T, ldv, device=dev, dtype=torch.bfloat16)[:, :V]
+K.lm_head_gemm("logits", h, w, lg, bias=torch.randn(V, device=dev, generator=g))
+dh = K.lm_head_gemm("dhidden", lg, w)
+gw = K.lm_head_gemm("dweight", lg, h)
+K.lm_head_gemm("dweight", lg, h, gw, accumulate=True)
+K.lm_head_backward(lg, h, w, grad_weight=torch.zeros(V, d, device=dev),
+                   grad_bias=torch.zeros(V, device=dev), accumulate=True)
+K.colsum(lg)
 torch.cuda.synchronize()
 print("sanitize smoke ok")
