@@ -36,8 +36,9 @@ extern "C" {
 #define AREAL_ABI_VERSION 1
 #define AREAL_N_STATS 8
 /* Workspace every K1/K2/K3 call needs (per concurrently used stream), zeroed once
- * at allocation.  K2 uses the lower half (ticket counter + per-CTA partials, left
- * zeroed after each launch), K3 the upper half (scratch). */
+ * at allocation.  K2 uses the lower half (ticket counter, row counter + per-CTA
+ * partials; the counters are re-armed by each launch's last CTA), K3 the upper half
+ * (scratch).  One workspace must not serve two launches running concurrently. */
 #define AREAL_WORKSPACE_BYTES (1u << 20)
 /* Largest number of sequences one minibatch may hold in the allocator. */
 #define AREAL_MAX_ITEMS_PER_MINIBATCH 8192
@@ -170,7 +171,10 @@ int areal_logprob_fwd(const void* logits, int64_t ld_logits, int dtype, int64_t 
  * the per-token part of _ppo_loss (198-213).  Writes dlogits (may alias
  * logits for an in-place backward), lp/entropy per token (either may be NULL)
  * and accumulates AREAL_N_STATS float64 statistics into `stats` (device).
- * Deterministic: per-CTA partials reduced in a fixed order. */
+ * Deterministic: per-CTA partials reduced in a fixed order; the TMEM kernel (16-bit
+ * rows, long fp32 rows) hands rows to CTAs dynamically and sums the objective /
+ * ratio / entropy in 128-bit fixed point, so its statistics do not depend on the
+ * row-to-CTA assignment either (bit-reproducible run to run). */
 int areal_ppo_fwd_bwd(const void* logits, int64_t ld_logits, void* dlogits, int64_t ld_dlogits,
                       int dtype, int64_t n_rows, int64_t vocab, const int64_t* tokens,
                       const double* behav, const double* prox, const double* adv,
