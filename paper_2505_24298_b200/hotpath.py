@@ -526,6 +526,7 @@ class DecoupledPPOStep:
         self.last_prox = prox
         mstats = torch.zeros((max(M, 1), K._lib.N_STATS), dtype=torch.float64, device=self.device)
         micro_count = 0
+        pending_reduce = []
         for m in range(M):
             st = mstats[m]
             for g, lo, hi in sp.mine[m]:
@@ -545,9 +546,18 @@ class DecoupledPPOStep:
                     backward_fn(m, g, dl)
             micro_count += int(sp.n_groups[m])
             if self.world > 1:
-                dist.all_reduce(st, group=self.group)           # the one collective
+                # the one collective; only the parameter update needs its result (its n_valid
+                # normaliser, trainer.py:329), so without one the next minibatch's kernels
+                # do not wait for it
+                work = dist.all_reduce(st, group=self.group, async_op=True)
+                if update_fn is not None:
+                    work.wait()
+                else:
+                    pending_reduce.append(work)
             if update_fn is not None:
                 update_fn(m, st)                                # 329-331
+        for work in pending_reduce:
+            work.wait()
         s = mstats[:M].cpu().numpy() if M else np.zeros((0, 8))
         tot = s.sum(axis=0) if M else np.zeros(8)
         d = max(int(tot[1]), 1)
