@@ -591,7 +591,8 @@ def run_ours(args, cfg):
                           achieved=k2_gbs, peak=peak, unit="GB/s", frac=k2_gbs / peak,
                           traffic=traffic, peak_source=peak_src,
                           algorithmic_bytes_per_token=2 * V * es + 52,
-                          launches=n_k2, avg_launch_ms=k2_ms / max(n_k2, 1)),
+                          launches=n_k2, avg_launch_ms=k2_ms / max(n_k2, 1),
+                          nominal_peak_gbs=8000.0, frac_of_nominal=k2_gbs / 8000.0),
             k1=dict(kernel="areal_logprob_fwd (K1)", achieved_gbs=k1_gbs, frac=k1_gbs / peak,
                     bytes_per_token=V * es + 16, ms_per_step=k1_ms / args.steps),
             k2=dict(ms_per_step=k2_ms / args.steps, tokens_per_s=T / (k2_ms / args.steps * 1e-3)),
