@@ -238,7 +238,10 @@ def _gemm_operands(op, M, N, K, dtype, seed, pad=0):
 
 @pytest.mark.parametrize("op", ["logits", "dhidden", "dweight"])
 @pytest.mark.parametrize("M,N,Kd", [(256, 256, 64), (300, 1000, 128), (1, 7, 64), (517, 333, 200),
-                                    (1024, 1536, 4096), (77, 4096, 1000)])
+                                    (1024, 1536, 4096), (77, 4096, 1000),
+                                    # odd N-tile counts: the second CTA pair of a 2x2 cluster
+                                    # computes a tile past N (zero B, clipped store)
+                                    (300, 700, 128), (640, 1200, 96)])
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
 def test_lm_head_gemm_matches_float64(op, M, N, Kd, dtype):
     """Each tcgen05 GEMM of the head (K-major / MN-major operands, tails of every tile
