@@ -11,13 +11,16 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--lib", default=None, help="a tuning build from tools/variants.py")
 ap.add_argument("--which", default="copy,k1,k2")
 ap.add_argument("--seconds", type=float, default=4.0)
+ap.add_argument("--rows", type=int, default=32768)
+ap.add_argument("--k2-variant", default="plain",
+                help="plain | gather (row_index permutation) | step (gather + versions + eta mask)")
 args = ap.parse_args()
 if args.lib:
     _lib.use_library(args.lib)
 from paper_2505_24298_b200 import kernels as K  # noqa: E402
 
 dev = torch.device("cuda", 0)
-T, V = 32768, 151936
+T, V = args.rows, 151936
 x = torch.empty(T, V, dtype=torch.bfloat16, device=dev).normal_(0, 2)
 y = torch.empty_like(x)
 tok = torch.randint(0, V, (T,), device=dev)
@@ -48,7 +51,7 @@ def run(fn, seconds=None):
     return s.elapsed_time(e) / n, n
 
 
-out = {"lib": args.lib}
+out = {"lib": args.lib, "rows": T, "k2_variant": args.k2_variant}
 which = args.which.split(",")
 if "copy" in which:
     ms, n = run(lambda: y.copy_(x))
@@ -57,7 +60,13 @@ if "k1" in which:
     ms, n = run(lambda: K.logprob_fwd(x, tok, lp_out=lp, with_entropy=False))
     out["k1"] = dict(ms=ms, iters=n, gbs=T * (V * 2 + 16) / ms / 1e6, **run.last_clock)
 if "k2" in which:
-    ms, n = run(lambda: K.ppo_fwd_bwd(x, tok, behav, lp, adv, dlogits=y, stats=stats))
+    kw = {}
+    if args.k2_variant in ("gather", "step"):
+        kw["row_index"] = torch.randperm(T, device=dev).to(torch.int32)
+    if args.k2_variant == "step":
+        kw.update(versions=torch.randint(90, 101, (T,), dtype=torch.int32, device=dev),
+                  current_version=100, eta_mask=8)
+    ms, n = run(lambda: K.ppo_fwd_bwd(x, tok, behav, lp, adv, dlogits=y, stats=stats, **kw))
     out["k2"] = dict(ms=ms, iters=n, gbs=T * (2 * V * 2 + 52) / ms / 1e6, **run.last_clock)
 if "copy" in which:
     ms, n = run(lambda: y.copy_(x))
