@@ -150,33 +150,33 @@ __device__ __forceinline__ void st_out(V* p, V v, bool stream) {
 constexpr int kRowQ = 16;
 static_assert(kRowQ >= 7 + 3 + 1, "row queue shorter than the producer's lead");
 // The objective / ratio / entropy sums are accumulated as 128-bit fixed point (2^-64
-// units): integer addition is associative, so the statistics do not depend on which CTA
+// units): each double is converted exactly (|x| < 2^62; bits below 2^-64 are floored),
+// integer addition is associative, so the statistics do not depend on which CTA
 // processed which rows (the row schedule is dynamic) and stay bit-reproducible.
 struct Fx128 {
-  unsigned long long lo;  // fraction, 2^-64 units
-  long long hi;           // integer part (two's complement with lo)
-  double nf;              // non-finite terms (inf / NaN), added as doubles
+  __int128 v;  // sum * 2^64
+  double nf;   // non-finite terms (inf / NaN), added as doubles
 };
-__device__ __forceinline__ void fx_add(Fx128& acc, unsigned long long lo, long long hi) {
-  const unsigned long long l = acc.lo + lo;
-  acc.hi += hi + (l < lo ? 1 : 0);
-  acc.lo = l;
-}
 __device__ __forceinline__ void fx_add(Fx128& acc, double x) {
   if (!isfinite(x)) {
     acc.nf += x;
     return;
   }
-  if (fabs(x) >= 0x1p62) {  // beyond the fixed-point range: keep it exact-order-free as inf
+  if (fabs(x) >= 0x1p62) {  // beyond the fixed-point range: counted as +-inf
     acc.nf += x > 0 ? INFINITY : -INFINITY;
     return;
   }
-  const double f = floor(x);
-  // x - f in [0, 1) is exact; scaled by 2^64 it is an exact double below 2^64
-  fx_add(acc, __double2ull_rz(ldexp(x - f, 64)), (long long)f);
+  int e;
+  const double m = frexp(x, &e);                  // x = m 2^e, |m| in [0.5, 1) or 0
+  const long long mi = (long long)ldexp(m, 53);   // exact 53-bit integer
+  const int sh = e - 53 + 64;                     // x 2^64 = mi 2^sh, sh <= 73
+  if (sh >= 0) acc.v += (__int128)mi << sh;
+  else if (sh > -64) acc.v += (__int128)mi >> (-sh);  // floor: deterministic
 }
 __device__ __forceinline__ double fx_value(const Fx128& acc) {
-  return ((double)acc.hi + ldexp((double)acc.lo, -64)) + acc.nf;
+  const long long hi = (long long)(acc.v >> 64);
+  const unsigned long long lo = (unsigned long long)acc.v;
+  return ((double)hi + ldexp((double)lo, -64)) + acc.nf;
 }
 struct TmemTail {
   int rowq[kRowQ];                            // row sequence (producer -> consumers)
@@ -232,8 +232,8 @@ __device__ void finalize_stats_fx(const PpoArgs& a, const TmemTail* tail) {
     for (int j = 0; j < AREAL_N_STATS; ++j) rec[j] = tail->st[j];
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
-      reinterpret_cast<unsigned long long*>(rec)[AREAL_N_STATS + 3 * j] = tail->fx[j].lo;
-      reinterpret_cast<long long*>(rec)[AREAL_N_STATS + 3 * j + 1] = tail->fx[j].hi;
+      reinterpret_cast<unsigned long long*>(rec)[AREAL_N_STATS + 3 * j] = (unsigned long long)tail->fx[j].v;
+      reinterpret_cast<long long*>(rec)[AREAL_N_STATS + 3 * j + 1] = (long long)(tail->fx[j].v >> 64);
       rec[AREAL_N_STATS + 3 * j + 2] = tail->fx[j].nf;
     }
     __threadfence();
@@ -253,11 +253,11 @@ __device__ void finalize_stats_fx(const PpoArgs& a, const TmemTail* tail) {
       v = 0.0;  // counters: integer-valued doubles, exact in any order
       for (unsigned int b = 0; b < gridDim.x; ++b) v += p[(size_t)b * kRec + j];
     } else {
-      Fx128 acc{0ull, 0ll, 0.0};
+      Fx128 acc{0, 0.0};
       const volatile unsigned long long* q = reinterpret_cast<const volatile unsigned long long*>(a.partials);
       for (unsigned int b = 0; b < gridDim.x; ++b) {
         const size_t o = (size_t)b * kRec + AREAL_N_STATS + 3 * f;
-        fx_add(acc, q[o], (long long)q[o + 1]);
+        acc.v += ((__int128)(long long)q[o + 1] << 64) | (__int128)q[o];
         acc.nf += p[o + 2];
       }
       v = fx_value(acc);
@@ -593,7 +593,7 @@ __device__ __forceinline__ void tmem_k2_body(const PpoArgs& a) {
     mbar_init(&tail->bcbar[0], 1);
     mbar_init(&tail->bcbar[1], 1);
     for (int j = 0; j < AREAL_N_STATS; ++j) tail->st[j] = 0.0;
-    for (int j = 0; j < 3; ++j) tail->fx[j] = Fx128{0ull, 0ll, 0.0};
+    for (int j = 0; j < 3; ++j) tail->fx[j] = Fx128{0, 0.0};
     tail->rowpub = 0u;
     fence_mbar_init_cluster();
   }
