@@ -996,9 +996,11 @@ extern "C" int areal_logprob_fwd(const void* logits, int64_t ld_logits, int dtyp
   if (n_rows < 0 || vocab < 1 || ld_logits < vocab) return AREAL_ERR_BAD_SHAPE;
   if (n_rows == 0) return AREAL_OK;
   if (!logits || !tokens || (!lp_out && !entropy_out)) return AREAL_ERR_INVALID_ARGUMENT;
-  (void)workspace;
-  (void)workspace_bytes;
   PpoArgs a = {};
+  // K1's ring kernel takes its rows from workspace counters when a workspace is given
+  // (static row order without one)
+  if (workspace && workspace_bytes >= AREAL_WORKSPACE_BYTES && n_rows < ((int64_t)1 << 31) - 4096)
+    a.counter = static_cast<unsigned int*>(workspace);
   a.logits = static_cast<const char*>(logits);
   a.ld_in_bytes = ld_logits * es;
   a.n_rows = n_rows;

@@ -41,7 +41,17 @@ struct RingBcast {
   int slow;                 // TMEM K2: statistics recomputed from HBM (fixed-shift overflow)
 };
 
+// K1 dynamic row schedule (single-CTA rows, workspace given): like the TMEM K2, the
+// producer claims each next row from a workspace counter and publishes the sequence
+// (rowq / rowpub); it runs at most nslots + 3 rows ahead of the epilogue.
+constexpr int kRingRowQ = 16;
+#ifndef AREAL_K1_DYNAMIC
+#define AREAL_K1_DYNAMIC 1
+#endif
+constexpr bool kK1Dynamic = AREAL_K1_DYNAMIC != 0;
 struct RingSmemTail {
+  int rowq[kRingRowQ];
+  unsigned int rowpub;
   uint64_t xbar[2];                 // DSMEM exchange barriers (double-buffered by row parity)
   uint64_t bcbar[2];                // epilogue -> math warps (double-buffered by row parity)
   double xval[2][8][3];             // [parity][rank][m, s, sx]
@@ -376,10 +386,27 @@ __device__ __forceinline__ void row_ring_body(const PpoArgs& a) {
     mbar_init(&tail->bcbar[0], 1);
     mbar_init(&tail->bcbar[1], 1);
     for (int j = 0; j < AREAL_N_STATS; ++j) tail->st[j] = 0.0;
+    tail->rowpub = 0u;
     fence_mbar_init_cluster();
   }
   __syncthreads();
   if (CS > 1) cluster_sync_all();  // peers' exchange barriers initialised before any remote arrive
+  // K1 on single-CTA rows takes its rows dynamically (workspace counters 2 and 3: next
+  // row, exit ticket); K2 on the ring keeps the static order its CTA-order statistics need
+  const bool dyn = kK1Dynamic && !BWD && CS == 1 && a.counter != nullptr;
+  unsigned int* const row_ctr = dyn ? a.counter + 2 : nullptr;
+  // it-th row of this CTA (-1: none left)
+  auto row_at = [&](int it) -> int64_t {
+    if (dyn) {
+      unsigned int pub;
+      do {
+        asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(pub) : "r"(smem_u32(&tail->rowpub)) : "memory");
+      } while (pub <= (unsigned int)it);
+      return tail->rowq[it % kRingRowQ];
+    }
+    const int64_t r = cid + (int64_t)it * ncl;
+    return r < a.n_rows ? r : -1;
+  };
 
   const int warp = tid >> 5, lane = tid & 31;
   if (warp == kProducerWarp) {
@@ -387,7 +414,15 @@ __device__ __forceinline__ void row_ring_body(const PpoArgs& a) {
     if (lane == 0) {
       Cursor cur = {0u, 0u};
       uint32_t used = 0;  // slots filled at least once (no wait needed on first use)
-      for (int64_t row = cid; row < a.n_rows; row += ncl) {
+      int64_t row = cid;
+      for (int k = 0;; ++k) {
+        if (dyn) {
+          tail->rowq[k % kRingRowQ] = row < a.n_rows ? (int)row : -1;
+          asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_u32(&tail->rowpub)), "r"((unsigned int)(k + 1))
+                       : "memory");
+        }
+        if (row >= a.n_rows) break;
+        const int64_t row_next = dyn ? ncl + (int64_t)atomicAdd(row_ctr, 1u) : row + ncl;
         const int hb = row_hb(row);
         const char* src = a.logits + row * a.ld_in_bytes + b16 * 16 - hb;
         for (int c = 0; c < nchunks; ++c) {
@@ -399,12 +434,14 @@ __device__ __forceinline__ void row_ring_body(const PpoArgs& a) {
                    &full[cur.slot]);
           cur.next(nslots);
         }
+        row = row_next;
       }
     }
   } else if (warp == kEpilogueWarp) {
     // ================= epilogue: merge, cluster exchange, fp64 per-token epilogue
-    int it = 0;
-    for (int64_t row = cid; row < a.n_rows; row += ncl, ++it) {
+    for (int it = 0;; ++it) {
+      const int64_t row = row_at(it);
+      if (row < 0) break;
       const int par = it & 1;
       // this row's token and scalars: plain loads issued now, consumed after the
       // math warps finish pass 1 (the warp is otherwise idle meanwhile)
@@ -506,8 +543,9 @@ __device__ __forceinline__ void row_ring_body(const PpoArgs& a) {
     carry.init();
     bool pending = false;      // BWD, lane 0: last store's slot not yet released
     uint32_t pend_slot = 0;
-    int it = 0;
-    for (int64_t row = cid; row < a.n_rows; row += ncl, ++it) {
+    for (int it = 0;; ++it) {
+      const int64_t row = row_at(it);
+      if (row < 0) break;
       const int par = it & 1;
       // ---- pass 1: online (max, sum e, sum e*x) over the chunks as they land
       RowStat<A> rs = carry;
@@ -653,6 +691,12 @@ __device__ __forceinline__ void row_ring_body(const PpoArgs& a) {
   }
   // all threads: final stats reduction (rank-0 CTAs carry the counters)
   __syncthreads();
+  if (dyn && threadIdx.x == 0) {  // the last CTA out re-arms the row counter
+    if (atomicAdd(a.counter + 3, 1u) == gridDim.x - 1) {
+      a.counter[2] = 0u;
+      a.counter[3] = 0u;
+    }
+  }
   if (BWD) {
     double cta[AREAL_N_STATS];
     for (int j = 0; j < AREAL_N_STATS; ++j) cta[j] = tail->st[j];
