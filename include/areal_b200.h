@@ -37,8 +37,10 @@ extern "C" {
 #define AREAL_N_STATS 8
 /* Workspace every K1/K2/K3 call needs (per concurrently used stream), zeroed once
  * at allocation.  K2 uses the lower half (ticket counter, row counter + per-CTA
- * partials; the counters are re-armed by each launch's last CTA), K3 the upper half
- * (scratch).  One workspace must not serve two launches running concurrently. */
+ * partials), K1 two more counters (its dynamic row schedule; without a workspace K1
+ * falls back to a static row order), all re-armed by each launch's last CTA; K3 the
+ * upper half (scratch).  One workspace must not serve two launches running
+ * concurrently. */
 #define AREAL_WORKSPACE_BYTES (1u << 20)
 /* Largest number of sequences one minibatch may hold in the allocator. */
 #define AREAL_MAX_ITEMS_PER_MINIBATCH 8192
