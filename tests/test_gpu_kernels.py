@@ -753,3 +753,49 @@ def test_unaligned_tmem_gather_prox_from_lp_versions():
     check_k2(dt, got, st.cpu().numpy(), ref, T)
     ok, err = rel_close(lp.cpu().numpy(), ref["lp"], TOL[dt])
     assert ok, err
+
+
+def _capture(fn):
+    """fn captured in a CUDA graph after one warm-up run on a side stream."""
+    st = torch.cuda.Stream()
+    st.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(st):
+        fn()
+    torch.cuda.current_stream().wait_stream(st)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        fn()
+    return g
+
+
+@pytest.mark.parametrize("rows", [48, 300])
+def test_dynamic_row_kernels_in_cuda_graphs(rows):
+    """K1 and the TMEM K2 take rows from workspace counters that each launch's last CTA
+    re-arms: replaying a captured graph several times gives results bit-identical to
+    eager launches (48 rows: K1 runs the 2-CTA cluster path; 300: dynamic rows)."""
+    V = 151936
+    g0 = torch.Generator(device="cuda").manual_seed(rows)
+    x = (torch.randn(rows, V, device="cuda", generator=g0) * 2).to(torch.bfloat16)
+    tok = torch.randint(0, V, (rows,), device="cuda", generator=g0)
+    lp_e, _ = K.logprob_fwd(x, tok, with_entropy=False)
+    behav = lp_e + 0.1 * torch.randn(rows, device="cuda", generator=g0, dtype=torch.float64)
+    adv = torch.randn(rows, device="cuda", generator=g0, dtype=torch.float64)
+    dl_e, st_e = K.ppo_fwd_bwd(x, tok, behav, lp_e, adv)
+    lp = torch.zeros(rows, dtype=torch.float64, device="cuda")
+    dl = torch.empty_like(x)
+    st = torch.zeros(8, dtype=torch.float64, device="cuda")
+
+    def step():
+        K.logprob_fwd(x, tok, lp_out=lp, with_entropy=False)
+        st.zero_()
+        K.ppo_fwd_bwd(x, tok, behav, lp_e, adv, dlogits=dl, stats=st)
+
+    g = _capture(step)
+    for _ in range(3):
+        lp.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(lp, lp_e)
+        assert torch.equal(st, st_e)
+        assert torch.equal(dl, dl_e)
