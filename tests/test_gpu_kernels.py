@@ -799,3 +799,19 @@ def test_dynamic_row_kernels_in_cuda_graphs(rows):
         assert torch.equal(lp, lp_e)
         assert torch.equal(st, st_e)
         assert torch.equal(dl, dl_e)
+
+
+@pytest.mark.parametrize("dt", ["bf16", "f32"])
+def test_zero_rows(dt):
+    """An empty micro-batch is a no-op: no rows, stats unchanged, lp untouched."""
+    V = 151936
+    x = torch.empty(0, V, dtype=DT[dt], device="cuda")
+    tok = torch.zeros(4, dtype=torch.int64, device="cuda")
+    z = torch.zeros(4, dtype=torch.float64, device="cuda")
+    lp = torch.full((4,), 3.0, dtype=torch.float64, device="cuda")
+    K.logprob_fwd(x, tok, row_index=torch.empty(0, dtype=torch.int32, device="cuda"), lp_out=lp,
+                  with_entropy=False)
+    assert bool((lp == 3.0).all())
+    st = torch.ones(8, dtype=torch.float64, device="cuda")
+    K.ppo_fwd_bwd(x, tok, z, z, z, row_index=torch.empty(0, dtype=torch.int32, device="cuda"), stats=st)
+    assert bool((st == 1.0).all())
