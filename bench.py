@@ -125,6 +125,70 @@ def fused_head_bench(cfg, dev, iters=5):
                 speedup_vs_unfused=base / fused)
 
 
+def head_backward_bench(cfg, dev, iters=2):
+    """Auxiliary measurement of K8 (backward half): the loss + backward
+    through the LM head on one full micro-batch of the config's shape in 8,192-token
+    chunks (hotpath.linear_ppo_fwd_bwd: LOGITS GEMM -> K2 in place -> grouped dH / dW ->
+    grad_b, this library's tcgen05 kernels only), against the same chunking with cuBLAS
+    GEMMs around K2.  Random hidden states / head weights."""
+    import torch
+    from paper_2505_24298_b200 import kernels as K
+    from paper_2505_24298_b200.hotpath import linear_ppo_fwd_bwd
+    C, V, d, chunk = cfg["budget"], cfg["vocab"], cfg["hidden"], 8192
+    g = torch.Generator(device=dev).manual_seed(12)
+    h = torch.randn(C, d, device=dev, generator=g).to(torch.bfloat16)
+    w = (torch.randn(V, d, device=dev, generator=g) / d ** 0.5 * 4).to(torch.bfloat16)
+    b = torch.randn(V, device=dev, generator=g)
+    tok = torch.randint(0, V, (C,), device=dev, generator=g)
+    behav = torch.full((C,), -12.0, dtype=torch.float64, device=dev)
+    prox = behav + 0.01
+    adv = torch.randn(C, dtype=torch.float64, device=dev, generator=g)
+    gw = torch.zeros(V, d, dtype=torch.float32, device=dev)
+    gb = torch.zeros(V, dtype=torch.float32, device=dev)
+    dh = torch.empty_like(h)
+    buf = torch.empty((chunk, V), dtype=h.dtype, device=dev)
+    st = torch.zeros(8, dtype=torch.float64, device=dev)
+    bb = b.to(torch.bfloat16)
+
+    def ours():
+        linear_ppo_fwd_bwd(h, w, tok, behav, prox, adv, bias=b, chunk_tokens=chunk,
+                           grad_weight=gw, grad_bias=gb)
+
+    def cublas():
+        for lo in range(0, C, chunk):
+            hi = min(C, lo + chunk)
+            lg = buf[: hi - lo]
+            torch.addmm(bb, h[lo:hi], w.t(), out=lg)
+            K.ppo_fwd_bwd(lg, tok, behav, prox, adv, row_index=torch.arange(
+                lo, hi, dtype=torch.int32, device=dev), dlogits=lg, stats=st)
+            torch.mm(lg, w, out=dh[lo:hi])
+            gw.add_(torch.mm(lg.t(), h[lo:hi], out_dtype=torch.float32))
+            gb.add_(lg.sum(dim=0, dtype=torch.float32))
+
+    def t(fn):
+        fn()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(iters):
+            fn()
+        e.record()
+        torch.cuda.synchronize()
+        return s.elapsed_time(e) / iters
+
+    mine = base = float("inf")
+    for _ in range(2):  # interleaved, best of 2 each: the same (power-capped) thermal state
+        mine = min(mine, t(ours))
+        base = min(base, t(cublas))
+    flop = 6.0 * C * V * d
+    return dict(path="hotpath.linear_ppo_fwd_bwd (K8 LOGITS + K2 + grouped dH/dW + colsum)",
+                tokens=C, vocab=V, hidden=d, chunk_tokens=chunk, ms=mine,
+                tflops_3gemm=flop / (mine * 1e-3) / 1e12, cublas_ms=base,
+                cublas="cuBLAS GEMMs (addmm, mm, mm) around the same K2 and column sums",
+                speedup_vs_cublas=base / mine,
+                timing="interleaved, best of 2 x %d iterations each" % iters)
+
+
 def lengths_label(cfg) -> str:
     if "pareto" in cfg:
         a, sc, cap, fl = cfg["pareto"]
@@ -630,6 +694,8 @@ def run_ours(args, cfg):
         )
         if world == 1 and "hidden" in cfg and not args.no_fused_head:
             line["fused_head"] = fused_head_bench(cfg, dev)
+        if world == 1 and "hidden" in cfg and not args.no_head_backward:
+            line["head_backward"] = head_backward_bench(cfg, dev)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -657,6 +723,8 @@ def main():
                     help="reference arm: skip the full cfg1 run on all host cores")
     ap.add_argument("--no-fused-head", action="store_true",
                     help="skip the auxiliary K7 fused LM-head measurement")
+    ap.add_argument("--no-head-backward", action="store_true",
+                    help="skip the auxiliary K8 loss + backward through the LM head measurement")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     ap.add_argument("--share-gpu", action="store_true",
                     help="all ranks on cuda:0 (functional multi-rank check on one GPU)")
