@@ -17,11 +17,13 @@
 //
 // One persistent kernel per op, CTA pairs (tcgen05 .cta_group::2, M = 256 per pair,
 // N = 256, K-slabs of 64), warp-specialised like K7 (linear_lp.cu): warp 0 issues TMA
-// loads into a 6-stage ring (both CTAs, completion on the leader's barrier), warp 1 of the
+// loads into a 6-stage ring (completion on the pair leader's barrier), warp 1 of the
 // leader issues the MMAs into two TMEM accumulators (2 x 256 columns), warps 2-9 drain an
-// accumulator (tcgen05.ld 32x32b: thread = row) while the next one is computed.  Output
-// tiles are rastered in groups of `group_m` M-tiles so the pairs in flight share their A
-// and B k-slabs in L2.
+// accumulator (tcgen05.ld 32x32b: thread = row) into shared-memory boxes written by TMA
+// tensor stores (f32 += by TMA reduce-add) while the next one is computed.  The backward
+// GEMMs run two pairs per 4-CTA cluster on one M-tile: the pairs' common A operand is
+// loaded once and multicast to both (see produce_unit).  Output tiles are rastered in
+// groups of `group_m` M-tiles so the clusters in flight share their k-slabs in L2.
 #include <algorithm>
 
 #include "tcgen05.cuh"
