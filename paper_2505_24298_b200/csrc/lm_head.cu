@@ -44,8 +44,14 @@ constexpr int UMMA_K = 16;
 #define LMH_TMA_STORE 1
 #endif
 constexpr bool kTmaStore = LMH_TMA_STORE != 0;
+// staging boxes per epilogue warp (2: the next box is written while the previous one's
+// TMA store still reads its buffer; costs a ring stage)
+#ifndef LMH_EPI_BUFS
+#define LMH_EPI_BUFS 1
+#endif
+constexpr int EPI_BUFS = LMH_EPI_BUFS;
 #ifndef LMH_STAGES
-#define LMH_STAGES (LMH_TMA_STORE ? 6 : 7)
+#define LMH_STAGES (LMH_TMA_STORE ? 7 - LMH_EPI_BUFS : 7)
 #endif
 constexpr int STAGES = LMH_STAGES;          // x 32 KB: the most that fits beside the barriers
                                              // (and the epilogue's staging boxes)
@@ -56,7 +62,7 @@ constexpr int MN_BLOCK = 64 * 128;           // one 64-element MN block of a 64-
 constexpr int EPI_SPLIT = 2;                 // epilogue warps per TMEM lane quarter
 constexpr int EPI_THREADS = 128 * EPI_SPLIT;
 constexpr int EPI_BOX = 32 * 128;            // one warp's staging box: 32 rows x 128 B
-constexpr int EPI_SMEM = kTmaStore ? (EPI_THREADS / 32) * EPI_BOX : 0;
+constexpr int EPI_SMEM = kTmaStore ? (EPI_THREADS / 32) * EPI_BOX * EPI_BUFS : 0;
 constexpr int SMEM = STAGES * STAGE + EPI_SMEM + 1024;  // + run-time 1024-B alignment
 constexpr int DB_WARPS = 4;                  // column-sum warps (grad_b fused into DWEIGHT)
 constexpr int DB_FIRST_WARP = 2 + EPI_THREADS / 32;
@@ -307,8 +313,8 @@ __global__ void __launch_bounds__(kind_threads(KIND), 1)
     const int half = (warp - 2) >> 2;
     const uint32_t lane_base = tbase + ((uint32_t)(q * 32) << 16);
     const uint32_t tempty0 = mapa_shared(smem_u32(&tempty[0]), 2u * pair);  // this pair's MMA issuer
-    unsigned char* stg = smem + (size_t)STAGES * STAGE + (size_t)(warp - 2) * EPI_BOX;  // 1024-B aligned
-    uint4* srow = reinterpret_cast<uint4*>(stg + lane * 128);
+    unsigned char* const stg0 = smem + (size_t)STAGES * STAGE + (size_t)(warp - 2) * EPI_BOX * EPI_BUFS;
+    uint32_t box = 0;  // boxes this warp has staged (buffer = box % EPI_BUFS)
     uint32_t acc = 0, acc_phase = 0;
     for (int u = unit0; u < a.n_units; u += unit_step) {
       const Tile t = unit_tile(a, u);
@@ -349,8 +355,10 @@ __global__ void __launch_bounds__(kind_threads(KIND), 1)
           // swizzled staging (16-byte chunk j of row r at j ^ (r & 7): conflict-free, the
           // layout the 128-byte-swizzle tensor map expects), then one box per warp; TMA
           // clips rows >= M and columns >= N
+          unsigned char* const stg = stg0 + (size_t)(box % EPI_BUFS) * EPI_BOX;  // 1024-B aligned
+          uint4* const srow = reinterpret_cast<uint4*>(stg + lane * 128);
           if (p.f32_out) {
-            if (lane == 0) bulk_wait_read<0>();  // the previous box left the staging buffer
+            if (lane == 0) bulk_wait_read<EPI_BUFS - 1>();  // this buffer's last box was read
             __syncwarp();
 #pragma unroll
             for (int j = 0; j < 8; ++j)
@@ -363,9 +371,10 @@ __global__ void __launch_bounds__(kind_threads(KIND), 1)
               else tma_store_2d(tmC, stg, (int32_t)c0, row0);
               bulk_commit();
             }
+            ++box;
           } else {  // 16-bit: two 32-column chunks per 64-column box
             if ((c & 1) == 0) {
-              if (lane == 0) bulk_wait_read<0>();
+              if (lane == 0) bulk_wait_read<EPI_BUFS - 1>();
               __syncwarp();
             }
 #pragma unroll
@@ -380,6 +389,7 @@ __global__ void __launch_bounds__(kind_threads(KIND), 1)
                 tma_store_2d(tmC, stg, (int32_t)(c0 - 32), row0);
                 bulk_commit();
               }
+              ++box;
             }
           }
         } else if (row < p.M && c0 < p.N) {
