@@ -21,6 +21,9 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
+from paper_2505_24298_b200 import _lib  # noqa: E402
+if "--lib" in sys.argv:  # a tuning build from tools/variants.py (before the first load)
+    _lib.use_library(sys.argv[sys.argv.index("--lib") + 1])
 from paper_2505_24298_b200 import kernels as K  # noqa: E402
 from paper_2505_24298_b200.hotpath import EmissionRecorder  # noqa: E402
 
@@ -30,6 +33,7 @@ ap.add_argument("--vocab", type=int, default=151936)
 ap.add_argument("--dim", type=int, default=1536)
 ap.add_argument("--iters", type=int, default=50)
 ap.add_argument("--out", default=None)
+ap.add_argument("--lib", default=None, help="a tuning build from tools/variants.py")
 a = ap.parse_args()
 
 dev = torch.device("cuda", 0)
