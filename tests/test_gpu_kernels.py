@@ -815,3 +815,25 @@ def test_zero_rows(dt):
     st = torch.ones(8, dtype=torch.float64, device="cuda")
     K.ppo_fwd_bwd(x, tok, z, z, z, row_index=torch.empty(0, dtype=torch.int32, device="cuda"), stats=st)
     assert bool((st == 1.0).all())
+
+
+@pytest.mark.parametrize("dt,V", [("bf16", 151937), ("bf16", 50257), ("f32", 151936)])
+def test_dynamic_rows_many_rows_per_cta_vs_oracle(dt, V):
+    """More rows than SMs (several rows per CTA from the dynamic schedule) on the aligned,
+    unaligned and streamed TMEM K2 and the K1 ring kernel: lp, entropy, counters and every
+    dlogits element against the float64 oracle."""
+    T = 400
+    logits, x64, tokens, behav, prox, adv = make_case(T, V, dt, seed=V % 97)
+    ref = O.surrogate_terms(x64, tokens, behav, prox, adv)
+    lp1, ent1 = K.logprob_fwd(logits.cuda(), cuda(tokens))
+    PY.check_lp(lp1.cpu().numpy(), O.token_logprobs(x64, tokens), what=f"K1 {dt} V={V}")
+    lp = torch.zeros(T, dtype=torch.float64, device="cuda")
+    ent = torch.zeros(T, dtype=torch.float64, device="cuda")
+    dl, st = K.ppo_fwd_bwd(logits.cuda(), cuda(tokens), cuda(behav), cuda(prox), cuda(adv),
+                           lp_out=lp, entropy_out=ent)
+    PY.check_lp(lp.cpu().numpy(), O.token_logprobs(x64, tokens), what=f"K2 lp {dt} V={V}")
+    assert np.allclose(ent.cpu().numpy(), O.token_entropy(x64), rtol=1e-4, atol=1e-4)
+    bnd = PY.boundary_tokens(ref, 0.2)
+    PY.check_counters(st.cpu().numpy(), ref["stats"], int(bnd.sum()), what=f"{dt} V={V}")
+    PY.check_dlogits(dl.double().cpu().numpy(), ref["dlogits"], ref["coef"], tokens, dt,
+                     skip_rows=bnd, what=f"K2 dlogits {dt} V={V}")
